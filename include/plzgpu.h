@@ -1,0 +1,169 @@
+/*
+ * plzgpu.h — C-ABI drop-in boundary of the B200-native GPULZ path.
+ *
+ * The reference (`plz`, /root/reference/proj) exposes its compress /
+ * decompress path as a C++ API.  This header is the
+ * language-neutral boundary underneath the B200 re-implementation of that API
+ * (include/plz/ headers): plain pointers and sizes, no torch or C++ types.
+ * Each entry point names the reference interface it replaces.
+ *
+ * Buffers: every `in` / `img` / `out` pointer may be HOST memory (pageable or
+ * pinned) or DEVICE memory on the context's GPU (cudaMalloc / torch CUDA
+ * tensors).  Host buffers are staged through the context; device buffers are
+ * used in place.  Streams are `cudaStream_t` passed as `void*` (NULL = the
+ * context's own stream).
+ *
+ * Errors: functions return a plzgpu_status and, when `err` is non-NULL, fill
+ * it.  Codes 1-4 correspond one-to-one to the reference's exception types
+ * (errors.hpp:10-41); byte_offset / chunk_index / token_index carry the same
+ * values the reference stores in plz::corruption_error.
+ *
+ * Threading: a context owns device scratch and one stream; use one context per
+ * host thread.  Calls on distinct contexts may run concurrently.
+ */
+#ifndef PLZGPU_H
+#define PLZGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PLZGPU_ABI_VERSION 1
+
+typedef enum plzgpu_status {
+    PLZGPU_OK = 0,
+    PLZGPU_VALIDATION = 1,          /* plz::validation_error        (errors.hpp:15) */
+    PLZGPU_UNSUPPORTED_FORMAT = 2,  /* plz::unsupported_format_error (errors.hpp:20) */
+    PLZGPU_CORRUPTION = 3,          /* plz::corruption_error         (errors.hpp:27) */
+    PLZGPU_CONTRACT = 4,            /* plz::contract_error           (errors.hpp:39) */
+    PLZGPU_CUDA = 5,                /* CUDA runtime failure (no reference equivalent) */
+    PLZGPU_CAPACITY = 6             /* caller's output buffer too small */
+} plzgpu_status;
+
+/* plz::Params (params.hpp:18-25).  min_match is derived by plzgpu_validate. */
+typedef struct plzgpu_params {
+    int32_t symbol_width; /* S: 1, 2 or 4 */
+    int32_t window;       /* W: 4..255 */
+    int32_t chunk_size;   /* C: 1024..16384 symbols, power of two, > W */
+    int32_t interval;     /* I: 1, 2, 4, 8, 16; divides C */
+    uint64_t block_bytes; /* bytes per container; multiple of C*S */
+    int32_t min_match;    /* derived: 2/S + 1 */
+    int32_t reserved;
+} plzgpu_params;
+
+/* plz::PipelineStats (pipeline.hpp:14-18).  max_cmp_per_pos is an
+ * instrumentation counter of the reference's CPU matcher; the GPU matcher
+ * reports 0. */
+typedef struct plzgpu_stats {
+    uint64_t max_cmp_per_pos;
+    uint64_t pointer_tokens;
+    uint64_t literal_tokens;
+} plzgpu_stats;
+
+typedef struct plzgpu_error {
+    int32_t code;
+    int32_t reserved;
+    uint64_t byte_offset; /* corruption_error::byte_offset (relative to the container) */
+    uint64_t chunk_index; /* UINT64_MAX when not applicable */
+    uint64_t token_index; /* UINT64_MAX when not applicable */
+    char message[240];    /* the reference's what() text */
+} plzgpu_error;
+
+/* plz::BlockPlan (partition.hpp:14-20) */
+typedef struct plzgpu_block_plan {
+    uint64_t byte_start;
+    uint64_t byte_len;
+    uint32_t num_chunks;
+    uint32_t last_chunk_len;
+    uint8_t tail_len;
+    uint8_t pad[7];
+} plzgpu_block_plan;
+
+typedef struct plzgpu_ctx plzgpu_ctx;
+
+/* ------------------------------------------------------------ host-side */
+
+int plzgpu_abi_version(void);
+
+/* replaces plz::validate (params.hpp:30, params.cpp:19-45) */
+int plzgpu_validate(const plzgpu_params* raw, plzgpu_params* out, plzgpu_error* err);
+
+/* replaces plz::level_to_window (params.hpp:33, params.cpp:47-55) */
+int plzgpu_level_to_window(int level, int32_t* window, plzgpu_error* err);
+
+/* replaces plz::plan (partition.hpp:28, partition.cpp:5-25).  Writes up to
+ * max_blocks entries and returns the total block count. */
+uint64_t plzgpu_plan(uint64_t total_bytes, const plzgpu_params* params,
+                     plzgpu_block_plan* blocks, uint64_t max_blocks);
+
+/* replaces plz::container_size (format.hpp:53-54, format.cpp:69-73) */
+uint64_t plzgpu_container_size(uint32_t num_chunks, uint64_t flag_total,
+                               uint64_t payload_total, uint8_t tail_len);
+
+/* Worst-case image size for n input bytes (every chunk all-literal).  An
+ * output buffer of this size never overflows. */
+uint64_t plzgpu_compress_bound(uint64_t n, const plzgpu_params* params);
+
+/* Host walk of a HOST image with read_container's checks (format.cpp:112-185):
+ * the decoded size of the longest prefix of containers that parse.  Sizes the
+ * output of plzgpu_decompress; the errors themselves come from decompress. */
+uint64_t plzgpu_decompressed_bound(const void* host_img, uint64_t len);
+
+/* -------------------------------------------------------------- device */
+
+int plzgpu_ctx_create(int device, plzgpu_ctx** out, plzgpu_error* err);
+void plzgpu_ctx_destroy(plzgpu_ctx* ctx);
+/* the context's stream as cudaStream_t */
+void* plzgpu_ctx_stream(plzgpu_ctx* ctx);
+/* number of kernels the last compress / decompress enqueued */
+int plzgpu_ctx_last_launches(plzgpu_ctx* ctx);
+
+/* Same quantity for a host OR device image (device: the parse kernel runs
+ * and one small result is read back). */
+int plzgpu_decompressed_size(plzgpu_ctx* ctx, const void* img, uint64_t len, uint64_t* out_len,
+                             void* stream, plzgpu_error* err);
+
+/* replaces plz::compress (pipeline.hpp:28-30, pipeline.cpp:88-99).
+ * Writes the bit-exact .plz image to out[0..*out_len).  Synchronous. */
+int plzgpu_compress(plzgpu_ctx* ctx, const plzgpu_params* params, const void* in,
+                    uint64_t n, void* out, uint64_t cap, uint64_t* out_len,
+                    plzgpu_stats* stats, void* stream, plzgpu_error* err);
+
+/* Stream-ordered variant for device-resident data: d_in and d_out are device
+ * pointers, cap >= plzgpu_compress_bound(n); the image length lands in the
+ * device word *d_out_len.  Returns after enqueueing; device-detected errors
+ * (4-byte table overflow) are reported by plzgpu_ctx_finish. */
+int plzgpu_compress_async(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* d_out, uint64_t cap, uint64_t* d_out_len,
+                          void* stream, plzgpu_error* err);
+
+/* replaces plz::decompress_bytes (decoder.hpp:42-43, decoder.cpp:129-141).
+ * Synchronous. */
+int plzgpu_decompress(plzgpu_ctx* ctx, const void* img, uint64_t len, void* out,
+                      uint64_t cap, uint64_t* out_len, void* stream, plzgpu_error* err);
+
+/* Stream-ordered variant: device image and output; the decoded length lands
+ * in *d_out_len.  Errors are reported by plzgpu_ctx_finish. */
+int plzgpu_decompress_async(plzgpu_ctx* ctx, const void* d_img, uint64_t len, void* d_out,
+                            uint64_t cap, uint64_t* d_out_len, void* stream,
+                            plzgpu_error* err);
+
+/* Waits for the context's last async operation on `stream` and reports its
+ * device-side errors (and, after a compress, its stats). */
+int plzgpu_ctx_finish(plzgpu_ctx* ctx, void* stream, plzgpu_stats* stats, plzgpu_error* err);
+
+/* replaces plz::decompress_chunk (decoder.hpp:25-28, decoder.cpp:70-90):
+ * decodes one chunk's flag/payload slices (host or device memory) into
+ * out[0 .. logical_len*S). */
+int plzgpu_decompress_chunk(plzgpu_ctx* ctx, const void* flags, uint64_t n_flags,
+                            const void* payload, uint64_t n_payload, uint64_t logical_len,
+                            const plzgpu_params* params, uint64_t chunk_index, void* out,
+                            plzgpu_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PLZGPU_H */

@@ -1,0 +1,510 @@
+// decode.cu — container parse + block-parallel chunk decode.
+//
+// Reference: format.cpp:112-185 (read_container: every structural check, in
+// order, with byte offsets relative to the container), decoder.cpp:22-90
+// (walk_tokens / decompress_chunk: MSB-first flags, [len][off] pointers,
+// forward overlapping copies, typed errors in walk order) and
+// decoder.cpp:102-141 (containers back to back, chunk k written at k*C*S,
+// tail appended).
+//
+// plz_parse_kernel: one CTA walks the container chain on the device (header
+// fields by one thread, table monotonicity by the whole CTA with a min-reduce
+// that keeps the reference's "first failing entry, payload before flag"
+// order) and emits one descriptor per container.  No host round trip.
+//
+// plz_decode_kernel: persistent grid, one warp per chunk.  A chunk is decoded
+// 32 tokens at a time: each lane takes one token's flag bit, warp scans turn
+// token kinds into payload offsets and token lengths into output positions,
+// the first failing token is found with a ballot, literals are scattered in
+// parallel and pointers replayed in token order (lanes copy one pointer's
+// symbols together; a malformed len > off replicates with period off, the
+// forward-copy semantics of decoder.cpp:80-84).  Chunks up to 8 KiB decode in
+// shared memory and leave with 128-bit stores.
+#include "common.cuh"
+
+namespace plzgpu {
+namespace {
+
+constexpr int kDecodeWarps = 8;
+constexpr uint32_t kDecodeSmem = 8192;  // bytes of output staging per warp
+
+__device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= uint32_t(d)) v += x;
+    }
+    return v;
+}
+
+// Output symbols of a chunk: aligned T elements, or byte-wise when the
+// destination is not S-aligned (containers after a tailed one in a
+// concatenated image).
+template <int S, bool kBytes>
+struct SymOut {
+    using T = typename Sym<S>::T;
+    uint8_t* p;
+    __device__ __forceinline__ T load(uint64_t i) const {
+        if constexpr (kBytes) {
+            T v = 0;
+#pragma unroll
+            for (int b = 0; b < S; ++b) v |= T(p[i * S + b]) << (8 * b);
+            return v;
+        } else {
+            return reinterpret_cast<const T*>(p)[i];
+        }
+    }
+    __device__ __forceinline__ void store(uint64_t i, T v) const {
+        if constexpr (kBytes) {
+#pragma unroll
+            for (int b = 0; b < S; ++b) p[i * S + b] = uint8_t(v >> (8 * b));
+        } else {
+            reinterpret_cast<T*>(p)[i] = v;
+        }
+    }
+};
+
+// Token walk of one chunk by one warp; decoded symbols go to out[0, L).
+// Returns a TokenErr and the failing token index (decoder.cpp:22-66 order).
+template <int S, bool kBytes>
+__device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_t nf,
+                                      const uint8_t* __restrict__ pay, uint64_t np, uint64_t L,
+                                      SymOut<S, kBytes> out, uint32_t lane, uint64_t* err_tok) {
+    using T = typename Sym<S>::T;
+    uint64_t written = 0, in = 0, t = 0;
+    while (written < L) {
+        const uint64_t tt = t + lane;
+        const bool hf = (tt >> 3) < nf;
+        const uint32_t bit = hf ? (uint32_t(flags[tt >> 3]) >> (7u - uint32_t(tt & 7u))) & 1u : 0u;
+        const uint32_t sz = bit ? 2u : uint32_t(S);
+        const uint64_t pin = in + warp_incl_scan_u32(sz, lane) - sz;
+        const bool has = pin + sz <= np;
+        uint32_t len = 0, off = 0;
+        if (bit && has) {
+            len = pay[pin];
+            off = pay[pin + 1];
+        }
+        const uint32_t adv = bit ? len : 1u;
+        const uint64_t pos = written + warp_incl_scan_u32(adv, lane) - adv;
+        const bool reached = pos < L;
+        uint32_t e = TE_OK;
+        if (!hf) e = TE_FLAGS_EXHAUSTED;
+        else if (!has) e = TE_PAYLOAD_EXHAUSTED;
+        else if (bit) {
+            if (len == 0 || off == 0) e = TE_ZERO_FIELD;
+            else if (off > pos) e = TE_OFFSET_BEFORE_START;
+            else if (pos + len > L) e = TE_OVERRUN;
+        }
+        const uint32_t m_end = __ballot_sync(0xffffffffu, !reached);
+        const uint32_t m_err = __ballot_sync(0xffffffffu, e != TE_OK && reached);
+        const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
+        const uint32_t first_err = m_err ? uint32_t(__ffs(m_err) - 1) : 32u;
+        if (first_err < first_end) {
+            *err_tok = t + first_err;
+            return __shfl_sync(0xffffffffu, e, first_err);
+        }
+        const bool act = lane < first_end;
+        if (act && !bit) {
+            T v = 0;
+#pragma unroll
+            for (int b = 0; b < S; ++b) v |= T(pay[pin + b]) << (8 * b);
+            out.store(pos, v);
+        }
+        __syncwarp();
+        uint32_t pm = __ballot_sync(0xffffffffu, act && bit);
+        while (pm) {
+            const int l = __ffs(pm) - 1;
+            pm &= pm - 1;
+            const uint64_t bp = __shfl_sync(0xffffffffu, pos, l);
+            const uint32_t bl = __shfl_sync(0xffffffffu, len, l);
+            const uint32_t bo = __shfl_sync(0xffffffffu, off, l);
+            for (uint32_t i = lane; i < bl; i += 32)
+                out.store(bp + i, out.load(bp - bo + (bl <= bo ? i : i % bo)));
+            __syncwarp();
+        }
+        const uint32_t la = first_end - 1;
+        written = __shfl_sync(0xffffffffu, pos + adv, la);
+        in = __shfl_sync(0xffffffffu, pin + sz, la);
+        t += first_end;
+    }
+    if (in != np) {
+        *err_tok = t;
+        return TE_TRAILING_PAYLOAD;
+    }
+    // padding bits after the last token must be zero (decoder.cpp:61-63)
+    const uint64_t b0 = t >> 3;
+    for (uint64_t base = b0; base < nf; base += 32) {
+        const uint64_t bi = base + lane;
+        uint32_t v = bi < nf ? flags[bi] : 0u;
+        if (bi == b0) v &= 0xffu >> uint32_t(t & 7u);
+        const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
+        if (m) {
+            const int l = __ffs(m) - 1;
+            const uint32_t vv = __shfl_sync(0xffffffffu, v, l);
+            *err_tok = 8 * (base + uint64_t(l)) + uint64_t(__clz(vv) - 24);
+            return TE_NONZERO_PADDING;
+        }
+    }
+    if (nf != ((t + 7) >> 3)) {
+        *err_tok = t;
+        return TE_FLAG_COUNT;
+    }
+    return TE_OK;
+}
+
+// ------------------------------------------------------------------ parse
+enum ParseErr : uint32_t {
+    PE_OK = 0,
+    PE_TRUNC_HEADER = 1,
+    PE_MAGIC = 2,
+    PE_VERSION = 3,
+    PE_RESERVED = 4,
+    PE_PARAMS = 5,
+    PE_TAIL = 6,
+    PE_TRUNC_TABLES = 7,
+    PE_PAYLOAD_MONO = 8,
+    PE_FLAG_MONO = 9,
+    PE_PAYLOAD_START = 10,
+    PE_FLAG_START = 11,
+    PE_TRUNC_STREAMS = 12,
+    PE_ORIG_SMALL = 13,
+    PE_ORIG_ALIGN = 14,
+    PE_NUM_CHUNKS = 15,
+    PE_CAPACITY = 16,
+    PE_DESC_FULL = 17,
+};
+
+__device__ __forceinline__ bool header_params_ok(uint32_t S, uint32_t W, uint32_t I, uint32_t C) {
+    if (S != 1 && S != 2 && S != 4) return false;
+    if (W < 4 || W > 255) return false;
+    if (C != 1024 && C != 2048 && C != 4096 && C != 8192 && C != 16384) return false;
+    if (C <= W) return false;
+    if (I != 1 && I != 2 && I != 4 && I != 8 && I != 16) return false;
+    return true;  // C % I == 0 and the default block_bytes follow from the sets
+}
+
+__global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
+    __shared__ uint64_t s_at, s_out, s_chunks, s_j, s_n, s_maxcb;
+    __shared__ unsigned long long s_bad;
+    __shared__ uint32_t s_stop;
+    const uint32_t tid = threadIdx.x;
+    ParseResult* res = a.result;
+    if (tid == 0) {
+        s_at = 0;
+        s_out = 0;
+        s_chunks = 0;
+        s_j = 0;
+        s_stop = 0;
+        s_maxcb = 0;
+        res->err_kind = PE_OK;
+    }
+    __syncthreads();
+    for (;;) {
+        if (tid == 0) {
+            s_bad = ~0ull;
+            const uint64_t at = s_at;
+            if (at >= a.img_len) {
+                s_stop = 1;
+            } else if (s_j >= a.desc_cap) {
+                res->err_kind = PE_DESC_FULL;
+                s_stop = 1;
+            } else {
+                const uint8_t* b = a.img + at;
+                const uint64_t size = a.img_len - at;
+                uint32_t err = PE_OK, aux = 0;
+                uint64_t eoff = 0;
+                if (size < 26) {
+                    err = PE_TRUNC_HEADER;
+                    eoff = size;
+                } else if (b[0] != 'P' || b[1] != 'L' || b[2] != 'Z' || b[3] != '1') {
+                    err = PE_MAGIC;
+                } else if (b[4] != 1) {
+                    err = PE_VERSION;
+                    aux = b[4];
+                } else if (b[8] != 0) {
+                    err = PE_RESERVED;
+                    eoff = 8;
+                } else if (!header_params_ok(b[5], b[6], b[7], ld_le32(b + 9))) {
+                    err = PE_PARAMS;
+                    eoff = 5;
+                } else if (b[25] >= b[5]) {
+                    err = PE_TAIL;
+                    eoff = 25;
+                } else {
+                    const uint64_t n = ld_le32(b + 21);
+                    if (size < 26 + 8 * (n + 1)) {
+                        err = PE_TRUNC_TABLES;
+                        eoff = size;
+                    } else {
+                        s_n = n;
+                    }
+                }
+                if (err != PE_OK) {
+                    res->err_kind = err;
+                    res->err_aux = aux;
+                    res->err_container = s_j;
+                    res->err_offset = eoff;
+                    res->hdr_S = b[5];
+                    res->hdr_W = b[6];
+                    res->hdr_I = b[7];
+                    res->hdr_C = size >= 13 ? ld_le32(b + 9) : 0;
+                    s_stop = 1;
+                }
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+        {
+            // ---- table monotonicity, first violation in (entry, payload-first) order
+            const uint8_t* ptab = a.img + s_at + 26;
+            const uint64_t n = s_n;
+            const uint8_t* ftab = ptab + 4 * (n + 1);
+            for (uint64_t i = tid; i < n; i += blockDim.x) {
+                if (ld_le32(ptab + 4 * (i + 1)) < ld_le32(ptab + 4 * i)) {
+                    atomicMin(&s_bad, 2 * i);
+                } else if (ld_le32(ftab + 4 * (i + 1)) < ld_le32(ftab + 4 * i)) {
+                    atomicMin(&s_bad, 2 * i + 1);
+                }
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const uint64_t at = s_at, n = s_n;
+            const uint8_t* b = a.img + at;
+            const uint64_t size = a.img_len - at;
+            const uint8_t* ptab = b + 26;
+            const uint8_t* ftab = ptab + 4 * (n + 1);
+            uint32_t err = PE_OK;
+            uint64_t eoff = 0;
+            const uint64_t S = b[5], C = ld_le32(b + 9), tail = b[25];
+            const uint64_t orig = ld_le64(b + 13);
+            const uint64_t ftot = ld_le32(ftab + 4 * n), ptot = ld_le32(ptab + 4 * n);
+            const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + tail;
+            if (s_bad != ~0ull) {
+                const uint64_t i = s_bad >> 1;
+                err = (s_bad & 1) ? PE_FLAG_MONO : PE_PAYLOAD_MONO;
+                eoff = (s_bad & 1) ? 26 + 4 * (n + 1) + 4 * (i + 1) : 26 + 4 * (i + 1);
+            } else if (ld_le32(ptab) != 0) {
+                err = PE_PAYLOAD_START;
+                eoff = 26;
+            } else if (ld_le32(ftab) != 0) {
+                err = PE_FLAG_START;
+                eoff = 26 + 4 * (n + 1);
+            } else if (size < need) {
+                err = PE_TRUNC_STREAMS;
+                eoff = size;
+            } else if (orig < tail) {
+                err = PE_ORIG_SMALL;
+                eoff = 13;
+            } else if ((orig - tail) % S != 0) {
+                err = PE_ORIG_ALIGN;
+                eoff = 13;
+            } else if (((orig - tail) / S + C - 1) / C != n) {
+                err = PE_NUM_CHUNKS;
+                eoff = 21;
+            } else if (s_out + orig > a.out_cap) {
+                err = PE_CAPACITY;
+            }
+            if (err != PE_OK) {
+                res->err_kind = err;
+                res->err_container = s_j;
+                res->err_offset = eoff;
+                s_stop = 1;
+            } else {
+                const uint64_t symbols = (orig - tail) / S;
+                ContainerDesc d;
+                d.img_off = at;
+                d.out_off = s_out;
+                d.chunk_base = s_chunks;
+                d.flags_off = at + 26 + 8 * (n + 1);
+                d.payload_off = d.flags_off + ftot;
+                d.original_len = orig;
+                d.num_chunks = uint32_t(n);
+                d.chunk_size = uint32_t(C);
+                d.last_len = n ? uint32_t(symbols - (n - 1) * C) : 0u;
+                d.S = uint8_t(S);
+                d.W = b[6];
+                d.I = b[7];
+                d.tail_len = uint8_t(tail);
+                a.desc[s_j] = d;
+                // raw tail straight to the output (decoder.cpp:123-125)
+                const uint8_t* ts = a.img + d.payload_off + ptot;
+                if (a.out)
+                    for (uint64_t i = 0; i < tail; ++i) a.out[s_out + orig - tail + i] = ts[i];
+                if (C * S > s_maxcb) s_maxcb = C * S;
+                s_at = at + need;
+                s_out += orig;
+                s_chunks += n;
+                s_j += 1;
+            }
+        }
+        __syncthreads();
+        if (s_stop) break;
+    }
+    if (tid == 0) {
+        res->n_containers = s_j;
+        res->total_chunks = s_chunks;
+        res->total_out = s_out;
+        res->max_chunk_bytes = s_maxcb;
+        if (a.out_len) *a.out_len = s_out;
+    }
+}
+
+// ----------------------------------------------------------------- decode
+template <int S>
+__device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const ContainerDesc& d,
+                                                     uint64_t k, uint8_t* stage, uint32_t lane,
+                                                     uint64_t* err_tok) {
+    // table entries k, k+1 of both tables: lanes 0-7 payload, 8-15 flags
+    const uint8_t* ptab = a.img + d.img_off + 26;
+    const uint8_t* ftab = ptab + 4 * (uint64_t(d.num_chunks) + 1);
+    uint32_t byte = 0;
+    if (lane < 8) byte = ptab[4 * k + lane];
+    else if (lane < 16) byte = ftab[4 * k + (lane - 8)];
+    uint32_t v = byte << (8 * (lane & 3u));
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    const uint32_t p0 = __shfl_sync(0xffffffffu, v, 0), p1 = __shfl_sync(0xffffffffu, v, 4);
+    const uint32_t f0 = __shfl_sync(0xffffffffu, v, 8), f1 = __shfl_sync(0xffffffffu, v, 12);
+    const uint64_t C = d.chunk_size;
+    const uint64_t L = (k + 1 == d.num_chunks) ? d.last_len : C;
+    uint8_t* dst = a.out + d.out_off + k * C * S;
+    const bool in_smem = C * S <= kDecodeSmem;
+    const uint8_t* fl = a.img + d.flags_off + f0;
+    const uint8_t* py = a.img + d.payload_off + p0;
+    uint64_t tok = 0;
+    uint32_t e;
+    if (in_smem)
+        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{stage}, lane,
+                                        &tok);
+    else if ((reinterpret_cast<uintptr_t>(dst) & (S - 1)) == 0)
+        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, lane,
+                                        &tok);
+    else
+        e = decode_chunk_warp<S, true>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, true>{dst}, lane,
+                                       &tok);
+    if (e == TE_OK && in_smem) {
+        __syncwarp();
+        const uint64_t bytes = L * S;
+        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+            uint4* d16 = reinterpret_cast<uint4*>(dst);
+            const uint4* s16 = reinterpret_cast<const uint4*>(stage);
+            for (uint64_t i = lane; i < (bytes >> 4); i += 32) d16[i] = s16[i];
+            for (uint64_t i = ((bytes >> 4) << 4) + lane; i < bytes; i += 32) dst[i] = stage[i];
+        } else {
+            for (uint64_t i = lane; i < bytes; i += 32) dst[i] = stage[i];
+        }
+    }
+    __syncwarp();
+    *err_tok = tok;
+    return e;
+}
+
+__device__ __forceinline__ uint64_t find_container(const ContainerDesc* desc, uint64_t nc,
+                                                   uint64_t g) {
+    uint64_t lo = 0, hi = nc - 1;  // last descriptor with chunk_base <= g
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi + 1) >> 1;
+        if (desc[mid].chunk_base <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uint64_t g,
+                                                        uint8_t* stage, uint32_t lane,
+                                                        uint64_t* k, uint64_t* tok) {
+    const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
+    *k = g - d.chunk_base;
+    switch (d.S) {
+        case 1: return decode_one_chunk<1>(a, d, *k, stage, lane, tok);
+        case 2: return decode_one_chunk<2>(a, d, *k, stage, lane, tok);
+        default: return decode_one_chunk<4>(a, d, *k, stage, lane, tok);
+    }
+}
+
+__global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = lane_id();
+    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kDecodeSmem;
+    const uint64_t total = a.result->total_chunks;
+    for (;;) {
+        uint64_t g = 0;
+        if (lane == 0) g = atomicAdd(a.work, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= total) break;
+        uint64_t k, tok;
+        const uint32_t e = decode_global_chunk(a, g, stage, lane, &k, &tok);
+        if (e != TE_OK && lane == 0) atomicMin(a.err_chunk, (unsigned long long)g);
+    }
+}
+
+// Error details of the lowest failing chunk (re-decoded by one warp).
+__global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* chunk,
+                                        uint64_t* token) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint64_t g = *a.err_chunk;
+    uint64_t k = 0, tok = 0;
+    const uint32_t e = decode_global_chunk(a, g, smem, lane_id(), &k, &tok);
+    if (lane_id() == 0) {
+        *code = e;
+        *chunk = k;
+        *token = tok;
+    }
+}
+
+__global__ void plz_decode_one_kernel(DecodeOneArgs a) {
+    const uint32_t lane = lane_id();
+    uint64_t tok = 0;
+    uint32_t e;
+    switch (a.S) {
+        case 1:
+            e = decode_chunk_warp<1, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
+                                           SymOut<1, true>{a.out}, lane, &tok);
+            break;
+        case 2:
+            e = decode_chunk_warp<2, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
+                                           SymOut<2, true>{a.out}, lane, &tok);
+            break;
+        default:
+            e = decode_chunk_warp<4, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
+                                           SymOut<4, true>{a.out}, lane, &tok);
+            break;
+    }
+    if (lane == 0) {
+        *a.err_code = e;
+        *a.err_token = tok;
+    }
+}
+
+}  // namespace
+
+int decode_ctas_per_sm() {
+    int blocks = 0;
+    const size_t smem = size_t(kDecodeWarps) * kDecodeSmem;
+    cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel, kDecodeWarps * 32,
+                                                  smem);
+    return blocks;
+}
+
+void launch_parse(const DecodeArgs& a, cudaStream_t st) {
+    plz_parse_kernel<<<1, 1024, 0, st>>>(a);
+}
+
+void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = size_t(kDecodeWarps) * kDecodeSmem;
+    cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    plz_decode_kernel<<<grid, kDecodeWarps * 32, smem, st>>>(a);
+}
+
+void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
+                         cudaStream_t st) {
+    plz_chunk_detail_kernel<<<1, 32, kDecodeSmem, st>>>(a, code, chunk, token);
+}
+
+void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {
+    plz_decode_one_kernel<<<1, 32, 0, st>>>(a);
+}
+
+}  // namespace plzgpu

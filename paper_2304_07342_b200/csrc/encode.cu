@@ -1,0 +1,231 @@
+// encode.cu — Kernel I: match + greedy token walk + encode, one warp per chunk.
+//
+// Reference contract:
+//   matcher.cpp:71-111   longest match over w in [max(0,p-W), p), length capped
+//                        at min(p-w, 255, n-p), ties to the largest offset;
+//   matcher.cpp:113-131  positions with p % I != 0 are forced literals;
+//   encoder.cpp:18-73    greedy walk from 0: pointer iff off != 0 and
+//                        len >= min_match, MSB-first flag bits, pointer wire
+//                        order [len][off], literal = the S raw bytes.
+//
+// B200 design.  A warp owns a chunk (dynamic scheduling over a persistent
+// grid).  The chunk's bytes arrive in shared memory by one TMA bulk copy
+// (cp.async.bulk + mbarrier).  A right-to-left ballot pass turns them into
+// packed (symbol, equal-run) cells so a single shared load per side advances
+// an lcp by a whole run (the run-skipping of matcher.cpp:42-59, exact with
+// runs capped at 255 because no match exceeds 255).  The walk then only
+// searches the positions it visits: the 32 lanes split the <= W window
+// candidates, prune against the warp's best with REDUX max, and the packed key
+// (len << 8 | off) makes max() reproduce the largest-offset tie-break.  Output
+// tokens are staged in shared memory and flushed with 128-bit stores into a
+// per-chunk slot; Kernel II/III compact them.
+#include "common.cuh"
+
+namespace plzgpu {
+namespace {
+
+// Longest common run-skipping prefix of positions w < p, capped at ub.
+template <int S>
+__device__ __forceinline__ int lcp_cells(const typename Sym<S>::Cell* __restrict__ cells, int w,
+                                         int p, int ub) {
+    int k = 0;
+    while (k < ub) {
+        const auto a = cells[w + k];
+        const auto b = cells[p + k];
+        if (a == b) {  // same symbol, same run: both runs end together
+            k += static_cast<int>(cell_run<S>(a));
+            continue;
+        }
+        if (cell_sym<S>(a) == cell_sym<S>(b)) {  // runs differ: mismatch at the shorter end
+            const uint32_t ra = cell_run<S>(a), rb = cell_run<S>(b);
+            k += static_cast<int>(ra < rb ? ra : rb);
+        }
+        break;
+    }
+    return k < ub ? k : ub;
+}
+
+// Warp-cooperative find_match at position p (p > 0).  Returns the packed key
+// (len << 8) | off of the winning candidate, 0 when no candidate matches.
+template <int S>
+__device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell* __restrict__ cells,
+                                                    int p, int n, int W, uint32_t lane) {
+    const int lim = p < W ? p : W;       // offsets 1..lim are in the window
+    const int cap = (n - p) < 255 ? (n - p) : 255;
+    uint32_t best = 0;
+    int o = lim - static_cast<int>(lane);  // lane's largest offset; then o-32, o-64, ...
+    if (o >= 1) {
+        const int ub = o < cap ? o : cap;
+        const int k = lcp_cells<S>(cells, p - o, p, ub);
+        if (k > 0) best = (uint32_t(k) << 8) | uint32_t(o);
+    }
+    best = __reduce_max_sync(0xffffffffu, best);
+    int bk = static_cast<int>(best >> 8);
+    for (o -= 32; o >= 1; o -= 32) {
+        const int ub = o < cap ? o : cap;
+        if (ub <= bk) break;  // ub only shrinks with o: nothing left can win
+        const int w = p - o;
+        // a candidate beating bk must also match at relative position bk
+        if (bk > 0 && cell_sym<S>(cells[w + bk]) != cell_sym<S>(cells[p + bk])) continue;
+        const int k = lcp_cells<S>(cells, w, p, ub);
+        if (k > bk) {  // smaller offsets only win on strictly longer matches
+            bk = k;
+            best = (uint32_t(k) << 8) | uint32_t(o);
+        }
+    }
+    return __reduce_max_sync(0xffffffffu, best);
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) plz_encode_kernel(EncodeArgs a) {
+    using T = typename Sym<S>::T;
+    using Cell = typename Sym<S>::Cell;
+    extern __shared__ __align__(16) uint8_t smem[];
+
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const int C = a.C;
+    const size_t per_warp = encode_warp_smem(C, S);
+    uint8_t* base = smem + per_warp * warp;
+    Cell* cells = reinterpret_cast<Cell*>(base);                       // C cells
+    uint8_t* pay = base + size_t(C) * sizeof(Cell);                    // C*S bytes (16B aligned)
+    uint8_t* flg = pay + size_t(C) * S;                                // C/8 bytes
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(flg + C / 8);         // 8B aligned (C/8 % 16 == 0)
+
+    if (lane == 0) mbar_init(mbar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    unsigned long long warp_ptr = 0, warp_tok = 0;  // stats, flushed once per warp
+
+    for (;;) {
+        uint64_t g = 0;
+        if (lane == 0) g = atomicAdd(a.work, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= a.n_chunks) break;
+
+        const int n = (g + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
+        const uint32_t nbytes = uint32_t(n) * S;
+        const uint8_t* src = a.in + g * uint64_t(C) * S;
+
+        // ---- stage the chunk's bytes into `pay` (reused as the raw buffer)
+        if (a.bulk_ok && (nbytes & 15u) == 0) {
+            fence_proxy_async_smem();  // prior generic reads of `pay` before the TMA write
+            __syncwarp();
+            if (lane == 0) bulk_g2s(pay, src, nbytes, mbar);
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        } else {
+            for (uint32_t i = lane; i < nbytes; i += 32) pay[i] = src[i];
+            __syncwarp();
+        }
+
+        // ---- packed (symbol, run) cells, right to left in 32-position words
+        const T* raw = reinterpret_cast<const T*>(pay);
+        uint32_t carry = 0;
+        for (int w = (n - 1) >> 5; w >= 0; --w) {
+            const int i = (w << 5) + static_cast<int>(lane);
+            const T v = i < n ? raw[i] : T(0);
+            const bool eq = (i + 1 < n) && raw[i + 1] == v;
+            const uint32_t m = __ballot_sync(0xffffffffu, eq);
+            const uint32_t sh = m >> lane;
+            uint32_t r;
+            if (sh == (0xffffffffu >> lane))
+                r = (32u - lane) + carry;  // run continues into the next word
+            else
+                r = static_cast<uint32_t>(__ffs(~sh));  // (#equal successors) + 1
+            r = r < 255u ? r : 255u;
+            carry = __shfl_sync(0xffffffffu, r, 0);
+            if (i < n) cells[i] = make_cell<S>(v, r);
+        }
+        __syncwarp();
+
+        // ---- greedy walk (encoder.cpp:25-41) with on-demand matching
+        const int I = a.I, W = a.W, min_match = a.min_match;
+        int p = 0;
+        uint32_t t = 0, pl = 0, fb = 0, nptr = 0;
+        while (p < n) {
+            uint32_t key = 0;
+            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<S>(cells, p, n, W, lane);
+            const uint32_t k = key >> 8, o = key & 255u;
+            const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
+            if (lane == 0) {
+                if (ptr) {
+                    pay[pl] = uint8_t(k);
+                    pay[pl + 1] = uint8_t(o);
+                } else {
+                    const T v = cell_sym<S>(cells[p]);
+#pragma unroll
+                    for (int b = 0; b < S; ++b) pay[pl + b] = uint8_t(v >> (8 * b));
+                }
+            }
+            if (ptr) fb |= 0x80u >> (t & 7u);
+            pl += ptr ? 2u : uint32_t(S);
+            nptr += ptr ? 1u : 0u;
+            p += ptr ? static_cast<int>(k) : 1;
+            if ((t & 7u) == 7u) {
+                if (lane == 0) flg[t >> 3] = uint8_t(fb);
+                fb = 0;
+            }
+            ++t;
+        }
+        if ((t & 7u) != 0 && lane == 0) flg[t >> 3] = uint8_t(fb);
+        __syncwarp();
+
+        // ---- flush to the chunk's staging slots with 128-bit stores
+        const uint32_t nf = (t + 7u) >> 3;
+        uint4* dp = reinterpret_cast<uint4*>(a.pay_slots + g * uint64_t(C) * S);
+        const uint4* sp = reinterpret_cast<const uint4*>(pay);
+        for (uint32_t i = lane; i < (pl + 15u) >> 4; i += 32) dp[i] = sp[i];
+        uint4* df = reinterpret_cast<uint4*>(a.flag_slots + g * uint64_t(C / 8));
+        const uint4* sf = reinterpret_cast<const uint4*>(flg);
+        for (uint32_t i = lane; i < (nf + 15u) >> 4; i += 32) df[i] = sf[i];
+        if (lane == 0) {
+            a.psize[g] = pl;
+            a.fsize[g] = nf;
+        }
+        warp_ptr += nptr;
+        warp_tok += t;
+        __syncwarp();
+    }
+    if (lane == 0 && warp_tok) {
+        atomicAdd(&a.stats[0], warp_ptr);
+        atomicAdd(&a.stats[1], warp_tok - warp_ptr);
+    }
+}
+
+}  // namespace
+
+int encode_ctas_per_sm(int S, int C, int warps_per_cta) {
+    int blocks = 0;
+    const size_t smem = encode_warp_smem(C, S) * warps_per_cta;
+    const void* fn = S == 1 ? (const void*)plz_encode_kernel<1>
+                   : S == 2 ? (const void*)plz_encode_kernel<2>
+                            : (const void*)plz_encode_kernel<4>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, warps_per_cta * 32, smem);
+    return blocks;
+}
+
+void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = encode_warp_smem(a.C, S) * a.warps_per_cta;
+    const dim3 block(a.warps_per_cta * 32);
+    switch (S) {
+        case 1:
+            cudaFuncSetAttribute(plz_encode_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+            plz_encode_kernel<1><<<grid, block, smem, st>>>(a);
+            break;
+        case 2:
+            cudaFuncSetAttribute(plz_encode_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+            plz_encode_kernel<2><<<grid, block, smem, st>>>(a);
+            break;
+        default:
+            cudaFuncSetAttribute(plz_encode_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+            plz_encode_kernel<4><<<grid, block, smem, st>>>(a);
+            break;
+    }
+}
+
+}  // namespace plzgpu

@@ -1,0 +1,797 @@
+// host.cpp — C-ABI implementation (include/plzgpu.h): parameter checks,
+// partition geometry, device scratch, kernel orchestration and the mapping of
+// device outcomes onto the reference's error types and messages.
+//
+// Reference behaviour mirrored here (paths under /root/reference/proj):
+//   params.cpp:19-55     validation order and messages, min_match = 2/S + 1
+//   partition.cpp:5-25   blocks of block_bytes, C-symbol chunks, raw tail
+//   pipeline.cpp:88-99   image = containers back to back; empty input -> empty
+//   scan.cpp:43-44       4-byte table overflow -> validation_error
+//   format.cpp:112-185   read_container messages / byte offsets
+//   decoder.cpp:13-18    "corrupt chunk K, token T: what"
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/plzgpu.h"
+#include "kernels.h"
+
+using namespace plzgpu;
+
+namespace {
+
+constexpr uint64_t kNoIndex = UINT64_MAX;
+
+int set_err(plzgpu_error* e, int code, uint64_t off, uint64_t chunk, uint64_t tok,
+            const char* fmt, ...) {
+    if (e) {
+        e->code = code;
+        e->reserved = 0;
+        e->byte_offset = off;
+        e->chunk_index = chunk;
+        e->token_index = tok;
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(e->message, sizeof e->message, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+void clear_err(plzgpu_error* e) {
+    if (e) {
+        std::memset(e, 0, sizeof *e);
+        e->chunk_index = kNoIndex;
+        e->token_index = kNoIndex;
+    }
+}
+
+int cuda_fail(plzgpu_error* e, cudaError_t c, const char* where) {
+    return set_err(e, PLZGPU_CUDA, 0, kNoIndex, kNoIndex, "CUDA error in %s: %s", where,
+                   cudaGetErrorString(c));
+}
+
+#define CK(call)                                                     \
+    do {                                                             \
+        const cudaError_t ck_ = (call);                              \
+        if (ck_ != cudaSuccess) return cuda_fail(err, ck_, #call);   \
+    } while (0)
+
+// ------------------------------------------------------------ validation
+int bad_field(plzgpu_error* e, const char* field, const char* legal) {
+    return set_err(e, PLZGPU_VALIDATION, 0, kNoIndex, kNoIndex, "invalid %s: legal range is %s",
+                   field, legal);
+}
+
+// params.cpp:19-45, same order, same messages
+int validate_fields(const plzgpu_params& p, plzgpu_error* e) {
+    if (p.symbol_width != 1 && p.symbol_width != 2 && p.symbol_width != 4)
+        return bad_field(e, "symbol_width", "{1,2,4}");
+    if (p.window < 4 || p.window > 255)
+        return bad_field(e, "window", "[4,255] (0 is reserved for no-match)");
+    switch (p.chunk_size) {
+        case 1024: case 2048: case 4096: case 8192: case 16384: break;
+        default: return bad_field(e, "chunk_size", "{1024,2048,4096,8192,16384}");
+    }
+    if (p.chunk_size <= p.window) return bad_field(e, "chunk_size", "greater than window");
+    switch (p.interval) {
+        case 1: case 2: case 4: case 8: case 16: break;
+        default: return bad_field(e, "interval", "{1,2,4,8,16}");
+    }
+    if (p.chunk_size % p.interval != 0) return bad_field(e, "interval", "a divisor of chunk_size");
+    const uint64_t cb = uint64_t(p.chunk_size) * uint64_t(p.symbol_width);
+    if (p.block_bytes == 0 || p.block_bytes % cb != 0)
+        return bad_field(e, "block_bytes", "a positive multiple of chunk_size*symbol_width");
+    return PLZGPU_OK;
+}
+
+// Whole-input chunk geometry (partition.cpp:5-25 folded over all blocks).
+struct Geometry {
+    uint64_t n_bytes = 0, n_blocks = 0, cpb = 0, n_chunks = 0;
+    uint32_t last_len = 0;
+};
+
+Geometry geometry(uint64_t n, const plzgpu_params& p) {
+    Geometry g;
+    const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
+    g.n_bytes = n;
+    if (n == 0) return g;
+    g.n_blocks = (n + p.block_bytes - 1) / p.block_bytes;
+    g.cpb = p.block_bytes / (C * S);
+    const uint64_t last_bytes = n - (g.n_blocks - 1) * p.block_bytes;
+    const uint64_t last_syms = last_bytes / S;
+    const uint64_t last_chunks = (last_syms + C - 1) / C;
+    g.n_chunks = (g.n_blocks - 1) * g.cpb + last_chunks;
+    g.last_len = last_chunks ? uint32_t(last_syms - (last_chunks - 1) * C) : uint32_t(C);
+    return g;
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// --------------------------------------------------------------- scratch
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        size_t want = std::max(bytes, cap + cap / 2);
+        want = (want + 255) & ~size_t(255);
+        const cudaError_t e = cudaMalloc(&p, want);
+        if (e == cudaSuccess) cap = want;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// Small device words written by the kernels, read back in one copy.
+struct Meta {
+    uint64_t img_len;
+    unsigned long long stats[2];
+    uint32_t overflow;
+    uint32_t detail_code;
+    uint64_t detail_chunk;
+    uint64_t detail_token;
+    unsigned long long err_chunk;
+    uint32_t work[4];
+    ParseResult parse;
+};
+
+enum LastOp { OP_NONE, OP_COMPRESS, OP_DECOMPRESS };
+
+}  // namespace
+
+struct plzgpu_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    DevBuf in, img, out, pay_slots, flag_slots, psize, fsize, p64, f64, status, agg, incl, desc;
+    DevBuf meta;
+    Meta* host_meta = nullptr;  // pinned
+    int last_launches = 0;
+    LastOp last_op = OP_NONE;
+    DecodeArgs last_decode{};
+};
+
+namespace {
+
+cudaStream_t pick(plzgpu_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+
+Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
+
+// Enqueue Kernels I-III for a device-resident input.  img must hold
+// compress_bound bytes; img_len receives the image length on the device.
+int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t n,
+                     uint8_t* img, uint64_t* d_img_len, cudaStream_t st, plzgpu_error* err) {
+    const Geometry g = geometry(n, p);
+    const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
+    const uint64_t G = g.n_chunks;
+    const uint64_t tiles = (G + kScanTile - 1) / kScanTile;
+    CK(c->pay_slots.ensure(G * C * S + 64));
+    CK(c->flag_slots.ensure(G * (C / 8) + 64));
+    CK(c->psize.ensure(G * 4 + 64));
+    CK(c->fsize.ensure(G * 4 + 64));
+    CK(c->p64.ensure((G + 1) * 8));
+    CK(c->f64.ensure((G + 1) * 8));
+    CK(c->status.ensure(tiles * 4 + 4));
+    CK(c->agg.ensure(tiles * 16 + 16));
+    CK(c->incl.ensure(tiles * 16 + 16));
+    Meta* m = dmeta(c);
+    CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
+    CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
+    int launches = 0;
+    if (G > 0) {
+        CK(cudaMemsetAsync(c->status.p, 0, tiles * 4, st));
+        // ---- Kernel I
+        EncodeArgs e{};
+        e.in = d_in;
+        e.pay_slots = c->pay_slots.as<uint8_t>();
+        e.flag_slots = c->flag_slots.as<uint8_t>();
+        e.psize = c->psize.as<uint32_t>();
+        e.fsize = c->fsize.as<uint32_t>();
+        e.stats = m->stats;
+        e.work = &m->work[0];
+        e.n_chunks = G;
+        e.last_len = g.last_len;
+        e.C = p.chunk_size;
+        e.W = p.window;
+        e.I = p.interval;
+        e.min_match = std::max(1, p.min_match);
+        e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
+        const size_t per_warp = encode_warp_smem(p.chunk_size, p.symbol_width);
+        int wpc = int(std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp)));
+        e.warps_per_cta = wpc;
+        int per_sm = encode_ctas_per_sm(p.symbol_width, p.chunk_size, wpc);
+        if (per_sm < 1) per_sm = 1;
+        uint64_t grid = uint64_t(c->sms) * uint64_t(per_sm);
+        const uint64_t need = (G + wpc - 1) / wpc;
+        if (grid > need) grid = need;
+        launch_encode(p.symbol_width, e, int(grid), st);
+        ++launches;
+        // ---- Kernel II
+        ScanArgs s{};
+        s.psize = e.psize;
+        s.fsize = e.fsize;
+        s.n = G;
+        s.P64 = c->p64.as<uint64_t>();
+        s.F64 = c->f64.as<uint64_t>();
+        s.status = c->status.as<uint32_t>();
+        s.agg = c->agg.as<ulonglong2>();
+        s.incl = c->incl.as<ulonglong2>();
+        s.tile_counter = &m->work[1];
+        launch_scan(s, st);
+        ++launches;
+    } else {
+        CK(cudaMemsetAsync(c->p64.p, 0, 8, st));
+        CK(cudaMemsetAsync(c->f64.p, 0, 8, st));
+    }
+    // ---- Kernel III + headers
+    AssembleArgs a{};
+    a.in = d_in;
+    a.pay_slots = c->pay_slots.as<uint8_t>();
+    a.flag_slots = c->flag_slots.as<uint8_t>();
+    a.psize = c->psize.as<uint32_t>();
+    a.fsize = c->fsize.as<uint32_t>();
+    a.P64 = c->p64.as<uint64_t>();
+    a.F64 = c->f64.as<uint64_t>();
+    a.img = img;
+    a.img_len = d_img_len;
+    a.overflow = &m->overflow;
+    a.n_bytes = n;
+    a.n_chunks = G;
+    a.cpb = g.cpb;
+    a.block_bytes = p.block_bytes;
+    a.n_blocks = g.n_blocks;
+    a.S = p.symbol_width;
+    a.W = p.window;
+    a.I = p.interval;
+    a.C = p.chunk_size;
+    if (G > 0) {
+        launch_assemble(a, st);
+        ++launches;
+    }
+    launch_headers(a, st);
+    ++launches;
+    CK(cudaGetLastError());
+    c->last_launches = launches;
+    c->last_op = OP_COMPRESS;
+    return PLZGPU_OK;
+}
+
+int overflow_error(plzgpu_error* err) {
+    return set_err(err, PLZGPU_VALIDATION, 0, kNoIndex, kNoIndex,
+                   "block too large: offsets exceed 4-byte table range");
+}
+
+int corrupt(plzgpu_error* e, const std::string& what, uint64_t off) {
+    return set_err(e, PLZGPU_CORRUPTION, off, kNoIndex, kNoIndex,
+                   "corrupt container: %s (byte %llu)", what.c_str(), (unsigned long long)off);
+}
+
+// Map a ParseResult error onto the reference's exception (format.cpp:112-185).
+int parse_error(const ParseResult& r, plzgpu_error* err) {
+    const uint64_t off = r.err_offset;
+    switch (r.err_kind) {
+        case 1: return corrupt(err, "truncated header", off);
+        case 2:
+            return set_err(err, PLZGPU_UNSUPPORTED_FORMAT, 0, kNoIndex, kNoIndex,
+                           "not a PLZ1 container (bad magic)");
+        case 3:
+            return set_err(err, PLZGPU_UNSUPPORTED_FORMAT, 0, kNoIndex, kNoIndex,
+                           "unsupported container version %u", r.err_aux);
+        case 4: return corrupt(err, "nonzero reserved byte", off);
+        case 5: {
+            plzgpu_params p{};
+            p.symbol_width = r.hdr_S;
+            p.window = r.hdr_W;
+            p.interval = r.hdr_I;
+            p.chunk_size = int32_t(r.hdr_C);
+            p.block_bytes = uint64_t(256) << 20;
+            plzgpu_error v;
+            clear_err(&v);
+            validate_fields(p, &v);
+            return corrupt(err, v.message, off);
+        }
+        case 6: return corrupt(err, "tail_len >= symbol_width", off);
+        case 7: return corrupt(err, "truncated offset tables", off);
+        case 8: return corrupt(err, "payload offsets not monotone", off);
+        case 9: return corrupt(err, "flag offsets not monotone", off);
+        case 10: return corrupt(err, "payload offsets must start at 0", off);
+        case 11: return corrupt(err, "flag offsets must start at 0", off);
+        case 12: return corrupt(err, "truncated streams", off);
+        case 13: return corrupt(err, "original_len too small", off);
+        case 14: return corrupt(err, "original_len not aligned to symbols", off);
+        case 15: return corrupt(err, "num_chunks inconsistent with original_len", off);
+        case 16:
+            return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                           "output buffer too small for the decoded image");
+        default:
+            return set_err(err, PLZGPU_CONTRACT, 0, kNoIndex, kNoIndex, "parse failure %u",
+                           r.err_kind);
+    }
+}
+
+const char* token_what(uint32_t code) {
+    switch (code) {
+        case TE_FLAGS_EXHAUSTED: return "flag bits exhausted";
+        case TE_PAYLOAD_EXHAUSTED: return "payload exhausted";
+        case TE_ZERO_FIELD: return "zero pointer field";
+        case TE_OFFSET_BEFORE_START: return "offset before chunk start";
+        case TE_OVERRUN: return "pointer overruns chunk";
+        case TE_TRAILING_PAYLOAD: return "trailing payload bytes";
+        case TE_NONZERO_PADDING: return "nonzero flag padding";
+        case TE_FLAG_COUNT: return "flag bytes inconsistent with token count";
+        default: return "unknown";
+    }
+}
+
+int token_error(uint32_t code, uint64_t chunk, uint64_t token, plzgpu_error* err) {
+    return set_err(err, PLZGPU_CORRUPTION, 0, chunk, token, "corrupt chunk %llu, token %llu: %s",
+                   (unsigned long long)chunk, (unsigned long long)token, token_what(code));
+}
+
+int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_t* d_out,
+                       uint64_t cap, uint64_t* d_out_len, cudaStream_t st, plzgpu_error* err) {
+    Meta* m = dmeta(c);
+    if (c->desc.cap < 64 * sizeof(ContainerDesc)) CK(c->desc.ensure(64 * sizeof(ContainerDesc)));
+    CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
+    CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk, st));
+    CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
+    DecodeArgs a{};
+    a.img = d_img;
+    a.img_len = len;
+    a.out = d_out;
+    a.out_cap = cap;
+    a.desc = c->desc.as<ContainerDesc>();
+    a.desc_cap = c->desc.cap / sizeof(ContainerDesc);
+    a.result = &m->parse;
+    a.out_len = d_out_len;
+    a.err_chunk = &m->err_chunk;
+    a.work = &m->work[2];
+    launch_parse(a, st);
+    int per_sm = decode_ctas_per_sm();
+    if (per_sm < 1) per_sm = 1;
+    launch_decode(a, c->sms * per_sm, st);
+    CK(cudaGetLastError());
+    c->last_launches = 2;
+    c->last_op = OP_DECOMPRESS;
+    c->last_decode = a;
+    return PLZGPU_OK;
+}
+
+// After a decompress has completed: report its error, if any, in the
+// reference's order (chunk errors of earlier containers before the parse
+// error of a later one).  Sets *grow when the descriptor table overflowed.
+int finish_decompress(plzgpu_ctx* c, cudaStream_t st, bool* grow, plzgpu_error* err) {
+    Meta h;
+    CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *grow = false;
+    if (h.err_chunk != ~0ull) {
+        Meta* m = dmeta(c);
+        launch_chunk_detail(c->last_decode, &m->detail_code, &m->detail_chunk, &m->detail_token, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return token_error(h.detail_code, h.detail_chunk, h.detail_token, err);
+    }
+    if (h.parse.err_kind == 17) {
+        *grow = true;
+        return PLZGPU_OK;
+    }
+    if (h.parse.err_kind != 0) return parse_error(h.parse, err);
+    return PLZGPU_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+int plzgpu_abi_version(void) { return PLZGPU_ABI_VERSION; }
+
+int plzgpu_validate(const plzgpu_params* raw, plzgpu_params* out, plzgpu_error* err) {
+    clear_err(err);
+    const int rc = validate_fields(*raw, err);
+    if (rc) return rc;
+    if (out) {
+        *out = *raw;
+        out->min_match = 2 / raw->symbol_width + 1;  // params.cpp:43
+    }
+    return PLZGPU_OK;
+}
+
+int plzgpu_level_to_window(int level, int32_t* window, plzgpu_error* err) {
+    clear_err(err);
+    static const int32_t w[] = {32, 64, 128, 255};  // params.cpp:47-55
+    if (level < 1 || level > 4) return bad_field(err, "level", "[1,4]");
+    *window = w[level - 1];
+    return PLZGPU_OK;
+}
+
+uint64_t plzgpu_plan(uint64_t total, const plzgpu_params* p, plzgpu_block_plan* blocks,
+                     uint64_t max_blocks) {
+    const uint64_t S = uint64_t(p->symbol_width), C = uint64_t(p->chunk_size);
+    uint64_t pos = 0, count = 0;
+    while (pos < total) {
+        plzgpu_block_plan b{};
+        b.byte_start = pos;
+        b.byte_len = std::min<uint64_t>(p->block_bytes, total - pos);
+        const uint64_t syms = b.byte_len / S;
+        b.tail_len = uint8_t(b.byte_len % S);
+        if (syms > 0) {
+            b.num_chunks = uint32_t((syms + C - 1) / C);
+            b.last_chunk_len = uint32_t(syms - uint64_t(b.num_chunks - 1) * C);
+        }
+        if (count < max_blocks && blocks) blocks[count] = b;
+        ++count;
+        pos += b.byte_len;
+        if (p->block_bytes == 0) break;
+    }
+    return count;
+}
+
+uint64_t plzgpu_container_size(uint32_t num_chunks, uint64_t flag_total, uint64_t payload_total,
+                               uint8_t tail_len) {
+    return 26 + 8 * (uint64_t(num_chunks) + 1) + flag_total + payload_total + tail_len;
+}
+
+uint64_t plzgpu_compress_bound(uint64_t n, const plzgpu_params* p) {
+    if (n == 0 || p->block_bytes == 0) return 0;
+    const uint64_t S = uint64_t(p->symbol_width);
+    const uint64_t nb = (n + p->block_bytes - 1) / p->block_bytes;
+    const Geometry g = geometry(n, *p);
+    // all-literal payload (< n) + ceil(len/8) flags per chunk + headers/tables + tails
+    return n + (n / S) / 8 + g.n_chunks + nb * 26 + 8 * (g.n_chunks + nb) + 16;
+}
+
+uint64_t plzgpu_decompressed_bound(const void* host_img, uint64_t len) {
+    // format.cpp:112-185 checks on the host bytes; stops at the first
+    // container that read_container would reject
+    const uint8_t* b = static_cast<const uint8_t*>(host_img);
+    uint64_t at = 0, total = 0;
+    auto u32 = [](const uint8_t* q) {
+        return uint64_t(q[0]) | (uint64_t(q[1]) << 8) | (uint64_t(q[2]) << 16) |
+               (uint64_t(q[3]) << 24);
+    };
+    while (at < len) {
+        const uint64_t size = len - at;
+        const uint8_t* h = b + at;
+        if (size < 26 || std::memcmp(h, "PLZ1", 4) != 0 || h[4] != 1 || h[8] != 0) break;
+        plzgpu_params p{};
+        p.symbol_width = h[5];
+        p.window = h[6];
+        p.interval = h[7];
+        p.chunk_size = int32_t(u32(h + 9));
+        p.block_bytes = uint64_t(256) << 20;
+        if (validate_fields(p, nullptr) != PLZGPU_OK || h[25] >= h[5]) break;
+        const uint64_t n = u32(h + 21);
+        if (size < 26 + 8 * (n + 1)) break;
+        const uint8_t* pt = h + 26;
+        const uint8_t* ft = pt + 4 * (n + 1);
+        bool mono = u32(pt) == 0 && u32(ft) == 0;
+        for (uint64_t i = 0; mono && i < n; ++i)
+            mono = u32(pt + 4 * (i + 1)) >= u32(pt + 4 * i) && u32(ft + 4 * (i + 1)) >= u32(ft + 4 * i);
+        if (!mono) break;
+        const uint64_t ptot = u32(pt + 4 * n), ftot = u32(ft + 4 * n);
+        const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + h[25];
+        if (size < need) break;
+        uint64_t orig = 0;
+        for (int i = 0; i < 8; ++i) orig |= uint64_t(h[13 + i]) << (8 * i);
+        const uint64_t S = h[5], C = uint64_t(p.chunk_size);
+        if (orig < h[25] || (orig - h[25]) % S != 0 || ((orig - h[25]) / S + C - 1) / C != n) break;
+        total += orig;
+        at += need;
+    }
+    return total;
+}
+
+int plzgpu_decompressed_size(plzgpu_ctx* c, const void* img, uint64_t len, uint64_t* out_len,
+                             void* stream, plzgpu_error* err) {
+    clear_err(err);
+    *out_len = 0;
+    if (len == 0) return PLZGPU_OK;
+    if (!is_device_ptr(img)) {
+        *out_len = plzgpu_decompressed_bound(img, len);
+        return PLZGPU_OK;
+    }
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    for (;;) {
+        if (c->desc.cap < 64 * sizeof(ContainerDesc)) CK(c->desc.ensure(64 * sizeof(ContainerDesc)));
+        Meta* m = dmeta(c);
+        CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
+        DecodeArgs a{};
+        a.img = static_cast<const uint8_t*>(img);
+        a.img_len = len;
+        a.out = nullptr;  // size-only walk: no tails copied
+        a.out_cap = UINT64_MAX;
+        a.desc = c->desc.as<ContainerDesc>();
+        a.desc_cap = c->desc.cap / sizeof(ContainerDesc);
+        a.result = &m->parse;
+        launch_parse(a, st);
+        CK(cudaGetLastError());
+        Meta h;
+        CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h.parse.err_kind == 17) {
+            CK(c->desc.ensure(c->desc.cap * 4));
+            continue;
+        }
+        *out_len = h.parse.total_out;
+        return PLZGPU_OK;
+    }
+}
+
+int plzgpu_ctx_create(int device, plzgpu_ctx** out, plzgpu_error* err) {
+    clear_err(err);
+    *out = nullptr;
+    plzgpu_ctx* c = new (std::nothrow) plzgpu_ctx();
+    if (!c) return set_err(err, PLZGPU_CUDA, 0, kNoIndex, kNoIndex, "out of host memory");
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = c->meta.ensure(sizeof(Meta));
+    if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_meta), sizeof(Meta));
+    if (e != cudaSuccess) {
+        plzgpu_ctx_destroy(c);
+        return cuda_fail(err, e, "plzgpu_ctx_create");
+    }
+    *out = c;
+    return PLZGPU_OK;
+}
+
+void plzgpu_ctx_destroy(plzgpu_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (DevBuf* b : {&c->in, &c->img, &c->out, &c->pay_slots, &c->flag_slots, &c->psize,
+                      &c->fsize, &c->p64, &c->f64, &c->status, &c->agg, &c->incl, &c->desc,
+                      &c->meta})
+        b->release();
+    if (c->host_meta) cudaFreeHost(c->host_meta);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+void* plzgpu_ctx_stream(plzgpu_ctx* c) { return c->stream; }
+
+int plzgpu_ctx_last_launches(plzgpu_ctx* c) { return c->last_launches; }
+
+int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, uint64_t n,
+                    void* out, uint64_t cap, uint64_t* out_len, plzgpu_stats* stats, void* stream,
+                    plzgpu_error* err) {
+    clear_err(err);
+    *out_len = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    if (n == 0) return PLZGPU_OK;  // empty input -> empty image (test_decoder.cpp:76-80)
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const uint8_t* d_in = static_cast<const uint8_t*>(in);
+    if (!is_device_ptr(in)) {
+        CK(c->in.ensure(n));
+        CK(cudaMemcpyAsync(c->in.p, in, n, cudaMemcpyHostToDevice, st));
+        d_in = c->in.as<uint8_t>();
+    }
+    const uint64_t bound = plzgpu_compress_bound(n, params);
+    const bool direct = is_device_ptr(out) && cap >= bound;
+    uint8_t* img = static_cast<uint8_t*>(out);
+    if (!direct) {
+        CK(c->img.ensure(bound));
+        img = c->img.as<uint8_t>();
+    }
+    Meta* m = dmeta(c);
+    rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
+    if (rc) return rc;
+    Meta* h = c->host_meta;
+    CK(cudaMemcpyAsync(h, m, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h->overflow) return overflow_error(err);
+    if (h->img_len > cap)
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                       "output buffer too small: need %llu bytes", (unsigned long long)h->img_len);
+    if (!direct) {
+        CK(cudaMemcpyAsync(out, img, h->img_len,
+                           is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaStreamSynchronize(st));
+    }
+    *out_len = h->img_len;
+    if (stats) {
+        stats->max_cmp_per_pos = 0;
+        stats->pointer_tokens = h->stats[0];
+        stats->literal_tokens = h->stats[1];
+    }
+    return PLZGPU_OK;
+}
+
+int plzgpu_compress_async(plzgpu_ctx* c, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* d_out, uint64_t cap, uint64_t* d_out_len, void* stream,
+                          plzgpu_error* err) {
+    clear_err(err);
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    if (cap < plzgpu_compress_bound(n, params))
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                       "async compress needs cap >= plzgpu_compress_bound");
+    if (n == 0) {
+        CK(cudaMemsetAsync(d_out_len, 0, 8, st));
+        Meta* m = dmeta(c);
+        CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
+        c->last_launches = 0;
+        c->last_op = OP_COMPRESS;
+        return PLZGPU_OK;
+    }
+    return enqueue_compress(c, *params, static_cast<const uint8_t*>(d_in), n,
+                            static_cast<uint8_t*>(d_out), d_out_len, st, err);
+}
+
+int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, uint64_t cap,
+                      uint64_t* out_len, void* stream, plzgpu_error* err) {
+    clear_err(err);
+    *out_len = 0;
+    if (len == 0) return PLZGPU_OK;
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const uint8_t* d_img = static_cast<const uint8_t*>(img);
+    if (!is_device_ptr(img)) {
+        CK(c->img.ensure(len));
+        CK(cudaMemcpyAsync(c->img.p, img, len, cudaMemcpyHostToDevice, st));
+        d_img = c->img.as<uint8_t>();
+    }
+    const bool direct = is_device_ptr(out) && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+    uint8_t* d_out = static_cast<uint8_t*>(out);
+    if (!direct) {
+        CK(c->out.ensure(cap + 16));
+        d_out = c->out.as<uint8_t>();
+    }
+    for (;;) {
+        int rc = enqueue_decompress(c, d_img, len, d_out, cap, nullptr, st, err);
+        if (rc) return rc;
+        bool grow = false;
+        rc = finish_decompress(c, st, &grow, err);
+        if (rc) return rc;
+        if (!grow) break;
+        CK(c->desc.ensure(c->desc.cap * 4));
+    }
+    Meta h;
+    CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t total = h.parse.total_out;
+    if (!direct && total) {
+        CK(cudaMemcpyAsync(out, d_out, total,
+                           is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaStreamSynchronize(st));
+    }
+    *out_len = total;
+    return PLZGPU_OK;
+}
+
+int plzgpu_decompress_async(plzgpu_ctx* c, const void* d_img, uint64_t len, void* d_out,
+                            uint64_t cap, uint64_t* d_out_len, void* stream, plzgpu_error* err) {
+    clear_err(err);
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    if (reinterpret_cast<uintptr_t>(d_out) & 15u)
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                       "async decompress needs a 16-byte aligned device output");
+    if (len == 0) {
+        CK(cudaMemsetAsync(d_out_len, 0, 8, st));
+        Meta* m = dmeta(c);
+        CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
+        CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk, st));
+        c->last_launches = 0;
+        c->last_op = OP_NONE;
+        return PLZGPU_OK;
+    }
+    return enqueue_decompress(c, static_cast<const uint8_t*>(d_img), len,
+                              static_cast<uint8_t*>(d_out), cap, d_out_len, st, err);
+}
+
+int plzgpu_ctx_finish(plzgpu_ctx* c, void* stream, plzgpu_stats* stats, plzgpu_error* err) {
+    clear_err(err);
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    if (c->last_op == OP_DECOMPRESS) {
+        bool grow = false;
+        const int rc = finish_decompress(c, st, &grow, err);
+        if (rc) return rc;
+        if (grow)
+            return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                           "too many containers for the async descriptor table; use "
+                           "plzgpu_decompress once to size it");
+        return PLZGPU_OK;
+    }
+    Meta* h = c->host_meta;
+    CK(cudaMemcpyAsync(h, c->meta.p, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c->last_op == OP_COMPRESS) {
+        if (h->overflow) return overflow_error(err);
+        if (stats) {
+            stats->max_cmp_per_pos = 0;
+            stats->pointer_tokens = h->stats[0];
+            stats->literal_tokens = h->stats[1];
+        }
+    }
+    return PLZGPU_OK;
+}
+
+int plzgpu_decompress_chunk(plzgpu_ctx* c, const void* flags, uint64_t n_flags,
+                            const void* payload, uint64_t n_payload, uint64_t logical,
+                            const plzgpu_params* params, uint64_t chunk_index, void* out,
+                            plzgpu_error* err) {
+    clear_err(err);
+    if (params->symbol_width != 1 && params->symbol_width != 2 && params->symbol_width != 4)
+        return bad_field(err, "symbol_width", "{1,2,4}");
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = c->stream;
+    const uint64_t S = uint64_t(params->symbol_width);
+    const uint64_t out_bytes = logical * S;
+    // stage everything in one device scratch: flags | payload | out
+    const uint64_t fo = 0, po = (n_flags + 15) & ~uint64_t(15);
+    const uint64_t oo = po + ((n_payload + 15) & ~uint64_t(15));
+    CK(c->in.ensure(oo + out_bytes + 16));
+    uint8_t* base = c->in.as<uint8_t>();
+    const bool dev_f = is_device_ptr(flags), dev_p = is_device_ptr(payload);
+    if (n_flags)
+        CK(cudaMemcpyAsync(base + fo, flags, n_flags,
+                           dev_f ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    if (n_payload)
+        CK(cudaMemcpyAsync(base + po, payload, n_payload,
+                           dev_p ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    Meta* m = dmeta(c);
+    DecodeOneArgs a{};
+    a.flags = base + fo;
+    a.n_flags = n_flags;
+    a.payload = base + po;
+    a.n_payload = n_payload;
+    a.logical = logical;
+    a.S = params->symbol_width;
+    a.out = base + oo;
+    a.err_code = &m->detail_code;
+    a.err_token = &m->detail_token;
+    launch_decode_one(a, st);
+    CK(cudaGetLastError());
+    c->last_launches = 1;
+    Meta h;
+    CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h.detail_code != TE_OK) return token_error(h.detail_code, chunk_index, h.detail_token, err);
+    if (out_bytes)
+        CK(cudaMemcpyAsync(out, base + oo, out_bytes,
+                           is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           st));
+    CK(cudaStreamSynchronize(st));
+    return PLZGPU_OK;
+}
+
+}  // extern "C"

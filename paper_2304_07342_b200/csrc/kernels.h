@@ -1,0 +1,156 @@
+// kernels.h — host-visible launchers and argument blocks of the sm_100a kernels.
+//
+//   Kernel I   plz_encode_kernel<S>     match + greedy token walk + encode, one warp per chunk
+//   Kernel II  plz_scan_kernel          decoupled look-back exclusive scan of (payload, flag) sizes
+//   Kernel III plz_assemble_kernel      tables + flag/payload streams into the image (128-bit stores)
+//              plz_headers_kernel       container headers, last table entries, tails, image length
+//   Decode     plz_parse_kernel         container-chain walk with the reference's checks
+//              plz_decode_kernel        block-parallel chunk decode, one warp per chunk
+//              plz_decode_one_kernel    single-chunk decode (decompress_chunk / error details)
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace plzgpu {
+
+// Device-side error codes of token walks (decoder.cpp:22-66 order).
+enum TokenErr : uint32_t {
+    TE_OK = 0,
+    TE_FLAGS_EXHAUSTED = 1,
+    TE_PAYLOAD_EXHAUSTED = 2,
+    TE_ZERO_FIELD = 3,
+    TE_OFFSET_BEFORE_START = 4,
+    TE_OVERRUN = 5,
+    TE_TRAILING_PAYLOAD = 6,
+    TE_NONZERO_PADDING = 7,
+    TE_FLAG_COUNT = 8,
+};
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;  // chunks per look-back tile
+
+// Per-warp shared-memory bytes of the encode kernel for chunk size C, width S.
+__host__ __device__ inline size_t encode_warp_smem(int C, int S) {
+    const size_t cell = S == 1 ? 2 : (S == 2 ? 4 : 8);
+    size_t b = size_t(C) * cell + size_t(C) * S + size_t(C) / 8 + 16;
+    return (b + 15) & ~size_t(15);
+}
+
+struct EncodeArgs {
+    const uint8_t* in;           // byte 0 of global chunk 0
+    uint8_t* pay_slots;          // chunk g payload staged at g * C * S
+    uint8_t* flag_slots;         // chunk g flags staged at g * C / 8
+    uint32_t* psize;             // per-chunk payload bytes
+    uint32_t* fsize;             // per-chunk flag bytes
+    unsigned long long* stats;   // [0] pointer tokens, [1] literal tokens
+    uint32_t* work;              // dynamic chunk counter (zeroed before launch)
+    uint64_t n_chunks;           // global chunk count
+    uint32_t last_len;           // logical symbols of global chunk n_chunks-1
+    int C, W, I, min_match;
+    int bulk_ok;                 // input base 16B-aligned: TMA bulk loads allowed
+    int warps_per_cta;
+};
+void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+int encode_ctas_per_sm(int S, int C, int warps_per_cta);
+
+struct ScanArgs {
+    const uint32_t* psize;
+    const uint32_t* fsize;
+    uint64_t n;                  // chunk count
+    uint64_t* P64;               // n+1 exclusive prefixes of payload sizes
+    uint64_t* F64;               // n+1 exclusive prefixes of flag sizes
+    uint32_t* status;            // per tile: 0 empty, 1 aggregate, 2 inclusive
+    ulonglong2* agg;             // per tile (payload, flag) aggregate
+    ulonglong2* incl;            // per tile inclusive prefix
+    uint32_t* tile_counter;      // zeroed before launch
+};
+void launch_scan(const ScanArgs& a, cudaStream_t st);
+
+// Geometry shared by Kernel III and the header kernel.  Containers 0..nb-2
+// hold cpb full chunks; the last holds n_chunks - (nb-1)*cpb.
+struct AssembleArgs {
+    const uint8_t* in;           // input byte 0 (tails)
+    const uint8_t* pay_slots;
+    const uint8_t* flag_slots;
+    const uint32_t* psize;
+    const uint32_t* fsize;
+    const uint64_t* P64;
+    const uint64_t* F64;
+    uint8_t* img;                // output image
+    uint64_t* img_len;           // device word: total image bytes
+    uint32_t* overflow;          // device word: 1 if a 4-byte table entry overflows
+    uint64_t n_bytes;            // input bytes
+    uint64_t n_chunks;
+    uint64_t cpb;                // chunks per full container
+    uint64_t block_bytes;
+    uint64_t n_blocks;
+    int S, W, I, C;
+};
+void launch_assemble(const AssembleArgs& a, cudaStream_t st);
+void launch_headers(const AssembleArgs& a, cudaStream_t st);
+
+// ------------------------------------------------------------- decode side
+struct ContainerDesc {
+    uint64_t img_off;            // container byte 0 in the image
+    uint64_t out_off;            // decoded byte 0 in the output
+    uint64_t chunk_base;         // global index of the container's chunk 0
+    uint64_t flags_off;          // absolute image offset of the flag stream
+    uint64_t payload_off;        // absolute image offset of the payload stream
+    uint64_t original_len;
+    uint32_t num_chunks;
+    uint32_t chunk_size;
+    uint32_t last_len;
+    uint8_t S, W, I, tail_len;
+};
+
+// Parse outcome (written by plz_parse_kernel).  err_kind values are listed in
+// host.cpp (format.cpp:112-185 order); err_* describe the first failing
+// container.
+struct ParseResult {
+    uint64_t n_containers;
+    uint64_t total_chunks;
+    uint64_t total_out;
+    uint32_t err_kind;
+    uint32_t err_aux;            // version byte for the version error
+    uint64_t err_container;
+    uint64_t err_offset;         // byte offset relative to that container
+    uint8_t hdr_S, hdr_W, hdr_I, pad0;
+    uint32_t hdr_C;              // raw header fields for the validation message
+    uint64_t max_chunk_bytes;
+};
+
+struct DecodeArgs {
+    const uint8_t* img;
+    uint64_t img_len;
+    uint8_t* out;
+    uint64_t out_cap;
+    ContainerDesc* desc;
+    uint64_t desc_cap;
+    ParseResult* result;
+    uint64_t* out_len;           // device word (async API)
+    unsigned long long* err_chunk;  // min failing global chunk (atomicMin), ~0 if none
+    uint32_t* work;
+};
+void launch_parse(const DecodeArgs& a, cudaStream_t st);
+void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
+// re-decodes chunk *a.err_chunk and reports (TokenErr, chunk within container, token)
+void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
+                         cudaStream_t st);
+int decode_ctas_per_sm();
+
+struct DecodeOneArgs {
+    const uint8_t* flags;
+    uint64_t n_flags;
+    const uint8_t* payload;
+    uint64_t n_payload;
+    uint64_t logical;
+    int S;
+    uint8_t* out;                // logical*S bytes (may be null for error-only runs)
+    uint32_t* err_code;          // TokenErr
+    uint64_t* err_token;
+};
+void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st);
+
+}  // namespace plzgpu

@@ -1,0 +1,216 @@
+"""GPU parity: the B200 path (through the C-ABI) against the reference.
+
+Checker: oracle/_ref (the reference library compiled from its own sources)
+when present, else the C restatement oracle/plz_oracle.c (pinned to the same
+reference by tests/test_oracle.py and tests/golden/).  Integer/byte work: the
+bar is bit-exact images, bit-exact round trips, and identical typed errors.
+"""
+import random
+
+import pytest
+
+import inputs
+import oracle as O
+from paper_2304_07342_b200 import plz
+
+pytestmark = pytest.mark.gpu
+
+
+def ref_compress(data, p):
+    op = O.make_params(p.symbol_width, p.window, p.chunk_size, p.interval, p.block_bytes,
+                       p.min_match)
+    if O.ref_available():
+        return O.ref_compress(data, op, 0, stats=True)
+    return O.compress_stats(data, op)
+
+
+def ref_decompress(img):
+    return O.ref_decompress(img, 0) if O.ref_available() else O.decompress(img)
+
+
+def P(S=2, W=128, C=2048, I=1, block_bytes=256 << 20):
+    return plz.validate(plz.Params(S, W, C, I, block_bytes))
+
+
+# ------------------------------------------------------------ known answers
+def test_known_answer_sixteen_equal_bytes():
+    # test_encoder.cpp:44-52: tokens L,L,L,P(3,3),P(6,6),P(4,12), flags 0x1C
+    img = plz.compress(b"\xab" * 16, P(1, 255, 1024))
+    assert len(img) == 52
+    assert img[-10:] == bytes([0x1C, 0xAB, 0xAB, 0xAB, 3, 3, 6, 6, 4, 12])
+    assert plz.decompress_bytes(img) == b"\xab" * 16
+
+
+def test_known_answer_four_u32_symbols():
+    # test_encoder.cpp:54-65: S=4 -> L, P(1,1), P(2,2); flags 0x60
+    data = bytes([0x11, 0x22, 0x33, 0x44]) * 4
+    img = plz.compress(data, P(4, 255, 1024))
+    assert img[-9:] == bytes([0x60, 0x11, 0x22, 0x33, 0x44, 1, 1, 2, 2])
+
+
+def test_known_answer_single_symbol_tail():
+    # 0x5A at S=2: no chunk, one tail byte -> 35-byte container
+    img = plz.compress(b"\x5a", P(2, 128, 2048))
+    assert img.hex() == ("504c5a31" "01" "02" "80" "01" "00" "00080000" "0100000000000000"
+                         "00000000" "01" "00000000" "00000000" "5a")
+    assert plz.decompress_bytes(img) == b"\x5a"
+
+
+def test_empty_input_is_empty_image():
+    assert plz.compress(b"", P()) == b""
+    assert plz.decompress_bytes(b"") == b""
+
+
+# -------------------------------------------------------- randomized parity
+GRID = [(S, W, C, I) for S in (1, 2, 4) for W in (4, 32, 64, 128, 255)
+        for C in (1024, 2048, 4096, 8192, 16384) for I in (1, 2, 4, 8, 16) if C > W]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_grid_bit_exact(seed):
+    rng = random.Random(1000 + seed)
+    for it in range(60):
+        S, W, C, I = rng.choice(GRID)
+        bb = C * S * rng.choice([1, 2, 3]) if rng.random() < 0.25 else 256 << 20
+        p = P(S, W, C, I, bb)
+        size = rng.choice([0, 1, S - 1, S, C * S - 1, C * S, C * S + 1, rng.randrange(1, 70000)])
+        kind = rng.choice(inputs.KINDS)
+        data = inputs.make(kind, size, seed * 1000 + it, S)
+        want, st_ref = ref_compress(data, p)
+        stats = plz.PipelineStats()
+        got = plz.compress(data, p, stats=stats)
+        assert got == want, f"image mismatch S={S} W={W} C={C} I={I} bb={bb} n={size} {kind}"
+        assert (stats.pointer_tokens, stats.literal_tokens) == st_ref[1:]
+        assert plz.decompress_bytes(got) == data
+        assert ref_decompress(got) == data
+
+
+@pytest.mark.parametrize("S,W,C,I", [(1, 128, 4096, 1), (2, 255, 2048, 2), (2, 255, 2048, 1),
+                                     (2, 255, 2048, 16), (4, 255, 1024, 4), (1, 255, 16384, 1),
+                                     (4, 255, 16384, 1), (2, 255, 8192, 8)])
+@pytest.mark.parametrize("kind", inputs.KINDS)
+def test_configs_bit_exact(S, W, C, I, kind):
+    data = inputs.make(kind, 3 * C * S + 777, hash((S, W, C, I, kind)) & 0xffff, S)
+    p = P(S, W, C, I)
+    want, _ = ref_compress(data, p)
+    got = plz.compress(data, p)
+    assert got == want
+    assert plz.decompress_bytes(got) == data
+
+
+def test_multi_block_images():
+    # test_decoder.cpp:198-207: two chunks per block, five blocks and a tail
+    p = P(2, 64, 1024, 1, 1024 * 2 * 2)
+    data = inputs.make("alpha", 5 * p.block_bytes + 777, 62, 2)
+    want, _ = ref_compress(data, p)
+    got = plz.compress(data, p)
+    assert got == want
+    assert plz.decompress_bytes(got) == data
+
+
+def test_concatenated_images_with_tails():
+    # containers with tails followed by more containers (odd output offsets)
+    parts = [inputs.make("alpha", n, n, 4) for n in (4099, 7, 12345, 3)]
+    imgs = [plz.compress(d, P(4, 255, 4096, 2)) for d in parts]
+    joined = b"".join(imgs)
+    assert plz.decompress_bytes(joined) == b"".join(parts)
+    assert ref_decompress(joined) == b"".join(parts)
+
+
+def test_device_resident_path_matches_host_path():
+    import torch
+
+    data = inputs.make("quant", 1 << 20, 5, 2)
+    p = P(2, 255, 2048, 2)
+    host = plz.compress(data, p)
+    d = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    dev = plz.compress(d, p)
+    assert dev.is_cuda and bytes(dev.cpu().numpy().tobytes()) == host
+    back = plz.decompress_bytes(dev)
+    assert back.is_cuda and torch.equal(back, d)
+
+
+# ---------------------------------------------------------------- errors
+def _err(fn, *a):
+    try:
+        fn(*a)
+    except plz.Error as e:
+        if isinstance(e, plz.CorruptionError):
+            return (type(e).__name__, str(e), e.byte_offset, e.chunk_index, e.token_index)
+        return (type(e).__name__, str(e), None, None, None)
+    except O.OracleError as e:
+        i = e.info
+        name = {1: "ValidationError", 2: "UnsupportedFormatError", 3: "CorruptionError",
+                4: "ContractError"}[i.code]
+        if i.code != O.CORRUPTION:
+            return (name, i.message, None, None, None)
+        chunk = None if i.chunk_index == O.NO_INDEX else i.chunk_index
+        tok = None if i.token_index == O.NO_INDEX else i.token_index
+        off = i.byte_offset if chunk is None else 0
+        return (name, i.message, off, chunk, tok)
+    return None
+
+
+def test_corrupted_images_raise_the_reference_error():
+    # test_decoder.cpp:260-279, strengthened: same type, message, offsets
+    rng = random.Random(66)
+    data = inputs.make("alpha", 30000, 66, 1)
+    p = P(1, 255, 1024, 1)
+    img = plz.compress(data, p)
+    same = 0
+    for it in range(300):
+        bad = bytearray(img)
+        for _ in range(rng.choice([1, 1, 2, 4])):
+            bad[rng.randrange(len(bad))] ^= rng.randrange(1, 256)
+        bad = bytes(bad)
+        mine = _err(plz.decompress_bytes, bad)
+        theirs = _err(ref_decompress, bad)
+        assert mine == theirs, f"iteration {it}"
+        if mine is None:
+            assert plz.decompress_bytes(bad) == ref_decompress(bad)
+        same += 1
+    assert same == 300
+
+
+def test_truncations_raise_the_reference_error():
+    data = inputs.make("runs", 20000, 3, 2)
+    img = plz.compress(data, P(2, 128, 1024, 1, 4096))
+    for cut in list(range(0, 80)) + list(range(len(img) - 40, len(img))):
+        assert _err(plz.decompress_bytes, img[:cut]) == _err(ref_decompress, img[:cut])
+
+
+def test_decompress_chunk_fuzz_matches_reference():
+    # test_decoder.cpp:242-258: random slices decode or raise a located error
+    rng = random.Random(65)
+    for it in range(400):
+        S = rng.choice([1, 2, 4])
+        p = P(S, 255, 1024)
+        op = O.make_params(S, 255, 1024, 1)
+        flags = bytes(rng.randrange(256) for _ in range(1 + rng.randrange(8)))
+        payload = bytes(rng.randrange(256) for _ in range(rng.randrange(64)))
+        logical = 1 + rng.randrange(200)
+        mine = _err(plz.decompress_chunk, flags, payload, logical, p, 7)
+        f = O.ref_decompress_chunk if O.ref_available() else O.decompress_chunk
+        theirs = _err(f, flags, payload, logical, op, 7)
+        assert mine == theirs
+        if mine is None:
+            assert plz.decompress_chunk(flags, payload, logical, p, 7) == f(flags, payload,
+                                                                            logical, op, 7)
+
+
+def test_overlapping_pointer_replicates_period():
+    # L L P(5,2) at S=2 replicates the period (decoder.cpp:80-84)
+    flags = bytes([0b00100000])
+    payload = bytes([1, 2, 3, 4, 5, 2])
+    p = P(2, 255, 1024)
+    got = plz.decompress_chunk(flags, payload, 7, p)
+    assert got == bytes([1, 2, 3, 4] * 3 + [1, 2])
+
+
+@pytest.mark.parametrize("field", ["symbol_width", "window", "chunk_size", "interval"])
+def test_invalid_params_raise_validation_error(field):
+    bad = {"symbol_width": 3, "window": 256, "chunk_size": 3000, "interval": 3}[field]
+    raw = plz.Params()
+    setattr(raw, field, bad)
+    with pytest.raises(plz.ValidationError):
+        plz.compress(b"abc", raw)
