@@ -10,8 +10,9 @@
  * Buffers: every `in` / `img` / `out` pointer may be HOST memory (pageable or
  * pinned) or DEVICE memory on the context's GPU (cudaMalloc / torch CUDA
  * tensors).  Host buffers are staged through the context; device buffers are
- * used in place.  Streams are `cudaStream_t` passed as `void*` (NULL = the
- * context's own stream).
+ * used in place.  Streams are `cudaStream_t` passed as `void*`; NULL is the
+ * legacy default stream (CUDA convention); plzgpu_ctx_stream() returns the
+ * context's private non-blocking stream.
  *
  * Errors: functions return a plzgpu_status and, when `err` is non-NULL, fill
  * it.  Codes 1-4 correspond one-to-one to the reference's exception types
@@ -162,6 +163,14 @@ int plzgpu_decompress_chunk(plzgpu_ctx* ctx, const void* flags, uint64_t n_flags
                             const void* payload, uint64_t n_payload, uint64_t logical_len,
                             const plzgpu_params* params, uint64_t chunk_index, void* out,
                             plzgpu_error* err);
+
+/* ------------------------------------------------------ profiling hook */
+
+/* Enqueue Kernel I (match + encode) alone on a device input, so its share of
+ * a compress can be timed with CUDA events (bench.py roofline).  No image is
+ * produced. */
+int plzgpu_profile_encode(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* stream, plzgpu_error* err);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ SIGNATURES = [
     ("plzgpu_decompress_async", C.c_int, [_VP, _VP, _U64, _VP, _U64, _VP, _VP, _E]),
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),
     ("plzgpu_decompress_chunk", C.c_int, [_VP, _VP, _U64, _VP, _U64, _U64, _P, _U64, _VP, _E]),
+    ("plzgpu_profile_encode", C.c_int, [_VP, _P, _VP, _U64, _VP, _E]),
 ]
 
 _lib = None

@@ -27,6 +27,7 @@ namespace {
 
 constexpr int kDecodeWarps = 8;
 constexpr uint32_t kDecodeSmem = 8192;  // bytes of output staging per warp
+constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144;  // + token table (16-B aligned)
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -64,12 +65,30 @@ struct SymOut {
     }
 };
 
+// Source position (relative) of position rel inside pointer entry e:
+// relpos - off + ((rel - relpos) mod off), i.e. rel - off for well-formed
+// pointers and LZ77-style replication when len > off (decoder.cpp:80-84).
+__device__ __forceinline__ int source_of(uint32_t e, uint32_t rel) {
+    const uint32_t rp = e >> 16, off = e & 0xffu;
+    const uint32_t d = rel - rp;
+    return int(rp) - int(off) + int(d < off ? d : d % off);
+}
+
 // Token walk of one chunk by one warp; decoded symbols go to out[0, L).
 // Returns a TokenErr and the failing token index (decoder.cpp:22-66 order).
+//
+// 32 tokens per batch: lane j takes token t+j's flag bit; warp scans turn
+// token kinds into payload offsets and token lengths into output positions;
+// the first failing token is found with a ballot.  Literals are written, then
+// the batch's output positions are filled in 32-wide waves: a pointer
+// position copies from its source, chasing back through pointers of the same
+// wave (earlier waves and literals are already final).  `tab` is the warp's
+// 33-entry token table in shared memory: relpos << 16 | is_ptr << 8 | off.
 template <int S, bool kBytes>
 __device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_t nf,
                                       const uint8_t* __restrict__ pay, uint64_t np, uint64_t L,
-                                      SymOut<S, kBytes> out, uint32_t lane, uint64_t* err_tok) {
+                                      SymOut<S, kBytes> out, uint32_t* tab, uint32_t lane,
+                                      uint64_t* err_tok) {
     using T = typename Sym<S>::T;
     uint64_t written = 0, in = 0, t = 0;
     while (written < L) {
@@ -77,7 +96,10 @@ __device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_
         const bool hf = (tt >> 3) < nf;
         const uint32_t bit = hf ? (uint32_t(flags[tt >> 3]) >> (7u - uint32_t(tt & 7u))) & 1u : 0u;
         const uint32_t sz = bit ? 2u : uint32_t(S);
-        const uint64_t pin = in + warp_incl_scan_u32(sz, lane) - sz;
+        // payload offset = 2 * (pointers before) + S * (literals before)
+        const uint32_t below = (1u << lane) - 1u;
+        const uint32_t nptr = __popc(__ballot_sync(0xffffffffu, bit) & below);
+        const uint64_t pin = in + 2u * nptr + uint32_t(S) * (lane - nptr);
         const bool has = pin + sz <= np;
         uint32_t len = 0, off = 0;
         if (bit && has) {
@@ -85,7 +107,8 @@ __device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_
             off = pay[pin + 1];
         }
         const uint32_t adv = bit ? len : 1u;
-        const uint64_t pos = written + warp_incl_scan_u32(adv, lane) - adv;
+        const uint32_t rel = warp_incl_scan_u32(adv, lane) - adv;  // < 32*255
+        const uint64_t pos = written + rel;
         const bool reached = pos < L;
         uint32_t e = TE_OK;
         if (!hf) e = TE_FLAGS_EXHAUSTED;
@@ -110,20 +133,39 @@ __device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_
             for (int b = 0; b < S; ++b) v |= T(pay[pin + b]) << (8 * b);
             out.store(pos, v);
         }
-        __syncwarp();
-        uint32_t pm = __ballot_sync(0xffffffffu, act && bit);
-        while (pm) {
-            const int l = __ffs(pm) - 1;
-            pm &= pm - 1;
-            const uint64_t bp = __shfl_sync(0xffffffffu, pos, l);
-            const uint32_t bl = __shfl_sync(0xffffffffu, len, l);
-            const uint32_t bo = __shfl_sync(0xffffffffu, off, l);
-            for (uint32_t i = lane; i < bl; i += 32)
-                out.store(bp + i, out.load(bp - bo + (bl <= bo ? i : i % bo)));
+        const uint32_t la = first_end - 1;
+        const uint32_t span = __shfl_sync(0xffffffffu, rel + adv, la);
+        const uint32_t pm = __ballot_sync(0xffffffffu, act && bit);
+        if (pm) {
+            tab[lane] = (rel << 16) | (bit << 8) | off;
+            __syncwarp();
+            for (uint32_t wbase = 0; wbase < span; wbase += 32) {
+                // covering token of wave position i: (tokens starting before the
+                // wave) + (token starts at <= i inside it) - 1
+                const uint32_t before =
+                    __popc(__ballot_sync(0xffffffffu, act && rel < wbase));
+                const uint32_t starts = __reduce_or_sync(
+                    0xffffffffu, (act && rel >= wbase && rel - wbase < 32u) ? 1u << (rel - wbase) : 0u);
+                const uint32_t q = wbase + lane;
+                if (q < span) {
+                    const uint32_t ent = tab[before + __popc(starts & ((2u << lane) - 1u)) - 1u];
+                    if (ent & 0x100u) {
+                        int src = source_of(ent, q);
+                        while (src >= int(wbase)) {  // source in this wave: chase it back
+                            const uint32_t i = uint32_t(src) - wbase;
+                            const uint32_t e2 = tab[before + __popc(starts & ((2u << i) - 1u)) - 1u];
+                            if (!(e2 & 0x100u)) break;  // a literal: already written
+                            src = source_of(e2, uint32_t(src));
+                        }
+                        out.store(written + q, out.load(uint64_t(int64_t(written) + src)));
+                    }
+                }
+                __syncwarp();
+            }
+        } else {
             __syncwarp();
         }
-        const uint32_t la = first_end - 1;
-        written = __shfl_sync(0xffffffffu, pos + adv, la);
+        written += span;
         in = __shfl_sync(0xffffffffu, pin + sz, la);
         t += first_end;
     }
@@ -374,15 +416,16 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     const uint8_t* py = a.img + d.payload_off + p0;
     uint64_t tok = 0;
     uint32_t e;
+    uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem);
     if (in_smem)
-        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{stage}, lane,
-                                        &tok);
+        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{stage}, tab,
+                                        lane, &tok);
     else if ((reinterpret_cast<uintptr_t>(dst) & (S - 1)) == 0)
-        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, lane,
-                                        &tok);
+        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, tab,
+                                        lane, &tok);
     else
-        e = decode_chunk_warp<S, true>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, true>{dst}, lane,
-                                       &tok);
+        e = decode_chunk_warp<S, true>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, true>{dst}, tab,
+                                       lane, &tok);
     if (e == TE_OK && in_smem) {
         __syncwarp();
         const uint64_t bytes = L * S;
@@ -426,7 +469,7 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
 __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = lane_id();
-    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kDecodeSmem;
+    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kDecodeWarpSmem;
     const uint64_t total = a.result->total_chunks;
     for (;;) {
         uint64_t g = 0;
@@ -454,21 +497,22 @@ __global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* 
 }
 
 __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
+    __shared__ uint32_t tab[33];
     const uint32_t lane = lane_id();
     uint64_t tok = 0;
     uint32_t e;
     switch (a.S) {
         case 1:
             e = decode_chunk_warp<1, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
-                                           SymOut<1, true>{a.out}, lane, &tok);
+                                           SymOut<1, true>{a.out}, tab, lane, &tok);
             break;
         case 2:
             e = decode_chunk_warp<2, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
-                                           SymOut<2, true>{a.out}, lane, &tok);
+                                           SymOut<2, true>{a.out}, tab, lane, &tok);
             break;
         default:
             e = decode_chunk_warp<4, true>(a.flags, a.n_flags, a.payload, a.n_payload, a.logical,
-                                           SymOut<4, true>{a.out}, lane, &tok);
+                                           SymOut<4, true>{a.out}, tab, lane, &tok);
             break;
     }
     if (lane == 0) {
@@ -481,7 +525,7 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 
 int decode_ctas_per_sm() {
     int blocks = 0;
-    const size_t smem = size_t(kDecodeWarps) * kDecodeSmem;
+    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
     cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel, kDecodeWarps * 32,
                                                   smem);
@@ -493,14 +537,14 @@ void launch_parse(const DecodeArgs& a, cudaStream_t st) {
 }
 
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = size_t(kDecodeWarps) * kDecodeSmem;
+    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
     cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     plz_decode_kernel<<<grid, kDecodeWarps * 32, smem, st>>>(a);
 }
 
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st) {
-    plz_chunk_detail_kernel<<<1, 32, kDecodeSmem, st>>>(a, code, chunk, token);
+    plz_chunk_detail_kernel<<<1, 32, kDecodeWarpSmem, st>>>(a, code, chunk, token);
 }
 
 void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {

@@ -24,11 +24,11 @@
 namespace plzgpu {
 namespace {
 
-// Longest common run-skipping prefix of positions w < p, capped at ub.
+// Continuation of an lcp once both positions sit at the same (symbol, run)
+// cell: both runs end together, so compare again at relative position k.
 template <int S>
-__device__ __forceinline__ int lcp_cells(const typename Sym<S>::Cell* __restrict__ cells, int w,
-                                         int p, int ub) {
-    int k = 0;
+__device__ __forceinline__ int lcp_continue(const typename Sym<S>::Cell* __restrict__ cells, int w,
+                                         int p, int k, int ub) {
     while (k < ub) {
         const auto a = cells[w + k];
         const auto b = cells[p + k];
@@ -46,38 +46,92 @@ __device__ __forceinline__ int lcp_cells(const typename Sym<S>::Cell* __restrict
 }
 
 // Warp-cooperative find_match at position p (p > 0).  Returns the packed key
-// (len << 8) | off of the winning candidate, 0 when no candidate matches.
+// (len << 8) | off of the winning candidate (len may be 0 = no match).
+//
+// Lane l evaluates offsets o = lim - l - 32r, r = 0..7, in branch-free
+// rounds: one shared load of the candidate's (symbol, run) cell settles it
+// unless the cell is identical to p's (same symbol, same remaining run) — a
+// different symbol gives 0, the same symbol with a different run length gives
+// min(run_w, run_p).  Identical cells (~15 of ~230 candidates on quant codes)
+// are only flagged in a per-lane bitmask and continued afterwards, so the
+// divergent continuation runs once per search instead of once per round.
+// One window candidate at offset o.  kCap: positions within 255 symbols of
+// the chunk end also cap the length at n - p; elsewhere min(len, o) <= 255
+// already.  Identical cells are flagged in `pending` for the continuation.
+template <int S, bool kCap>
+__device__ __forceinline__ void eval_candidate(typename Sym<S>::Cell cw, typename Sym<S>::Cell cp,
+                                               uint32_t rp, uint32_t o, uint32_t cap,
+                                               uint32_t bit, uint32_t& best, uint32_t& pending) {
+    using Cell = typename Sym<S>::Cell;
+    constexpr Cell kSymMask = (Cell(1) << (8 * S)) - 1;
+    const uint32_t rw = cell_run<S>(cw);
+    const uint32_t ub = kCap ? (o < cap ? o : cap) : o;
+    uint32_t k = rw < rp ? rw : rp;  // same symbol: the shorter run ends first
+    k = k < ub ? k : ub;
+    const uint32_t key = ((cw ^ cp) & kSymMask) == 0 ? (k << 8) | o : o;
+    best = key > best ? key : best;
+    if (cw == cp) pending |= bit;
+}
+
+// All candidates of one search: rounds 0..full-1 have every lane valid, the
+// tail round only lanes with offset >= 1.  The switch enters a straight-line
+// unrolled sequence (no per-round branches).
+template <int S, bool kCap>
+__device__ __forceinline__ void eval_window(const typename Sym<S>::Cell* __restrict__ cw,
+                                            typename Sym<S>::Cell cp, uint32_t rp, int o0,
+                                            int full, uint32_t cap, uint32_t& best,
+                                            uint32_t& pending) {
+#define PLZ_ROUND(R) \
+    eval_candidate<S, kCap>(cw[32 * (R)], cp, rp, uint32_t(o0 - 32 * (R)), cap, 1u << (R), best, pending)
+    switch (full) {
+        case 8: PLZ_ROUND(7); [[fallthrough]];
+        case 7: PLZ_ROUND(6); [[fallthrough]];
+        case 6: PLZ_ROUND(5); [[fallthrough]];
+        case 5: PLZ_ROUND(4); [[fallthrough]];
+        case 4: PLZ_ROUND(3); [[fallthrough]];
+        case 3: PLZ_ROUND(2); [[fallthrough]];
+        case 2: PLZ_ROUND(1); [[fallthrough]];
+        case 1: PLZ_ROUND(0); [[fallthrough]];
+        default: break;
+    }
+#undef PLZ_ROUND
+    if (full < 8 && o0 - 32 * full >= 1)
+        eval_candidate<S, kCap>(cw[32 * full], cp, rp, uint32_t(o0 - 32 * full), cap, 1u << full,
+                                best, pending);
+}
+
 template <int S>
 __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell* __restrict__ cells,
                                                     int p, int n, int W, uint32_t lane) {
-    const int lim = p < W ? p : W;       // offsets 1..lim are in the window
-    const int cap = (n - p) < 255 ? (n - p) : 255;
-    uint32_t best = 0;
-    int o = lim - static_cast<int>(lane);  // lane's largest offset; then o-32, o-64, ...
-    if (o >= 1) {
-        const int ub = o < cap ? o : cap;
-        const int k = lcp_cells<S>(cells, p - o, p, ub);
-        if (k > 0) best = (uint32_t(k) << 8) | uint32_t(o);
-    }
-    best = __reduce_max_sync(0xffffffffu, best);
-    int bk = static_cast<int>(best >> 8);
-    for (o -= 32; o >= 1; o -= 32) {
-        const int ub = o < cap ? o : cap;
-        if (ub <= bk) break;  // ub only shrinks with o: nothing left can win
-        const int w = p - o;
-        // a candidate beating bk must also match at relative position bk
-        if (bk > 0 && cell_sym<S>(cells[w + bk]) != cell_sym<S>(cells[p + bk])) continue;
-        const int k = lcp_cells<S>(cells, w, p, ub);
-        if (k > bk) {  // smaller offsets only win on strictly longer matches
-            bk = k;
-            best = (uint32_t(k) << 8) | uint32_t(o);
-        }
+    using Cell = typename Sym<S>::Cell;
+    const int lim = p < W ? p : W;  // offsets 1..lim are in the window
+    const uint32_t cap = uint32_t((n - p) < 255 ? (n - p) : 255);
+    const Cell cp = cells[p];
+    const uint32_t rp = cell_run<S>(cp);
+    const int o0 = lim - static_cast<int>(lane);  // round r: offset o0 - 32r
+    const Cell* cw = cells + (p - o0);              // round r: cw[32r]
+    const int full = lim >> 5;                      // rounds where every lane is valid
+    uint32_t best = 0, pending = 0;
+    if (cap == 255)
+        eval_window<S, false>(cw, cp, rp, o0, full, cap, best, pending);
+    else
+        eval_window<S, true>(cw, cp, rp, o0, full, cap, best, pending);
+    // identical cells: both runs end together, continue at relative rp
+    while (pending) {
+        const int r = __ffs(pending) - 1;
+        pending &= pending - 1;
+        const int o = o0 - 32 * r;
+        const int ub = o < int(cap) ? o : int(cap);
+        if (int(rp) >= ub) continue;
+        const uint32_t k = uint32_t(lcp_continue<S>(cells, p - o, p, static_cast<int>(rp), ub));
+        const uint32_t key = (k << 8) | uint32_t(o);
+        best = key > best ? key : best;
     }
     return __reduce_max_sync(0xffffffffu, best);
 }
 
 template <int S>
-__global__ void __launch_bounds__(256) plz_encode_kernel(EncodeArgs a) {
+__global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     using T = typename Sym<S>::T;
     using Cell = typename Sym<S>::Cell;
     extern __shared__ __align__(16) uint8_t smem[];

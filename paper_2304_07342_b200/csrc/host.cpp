@@ -174,18 +174,23 @@ struct plzgpu_ctx {
     int last_launches = 0;
     LastOp last_op = OP_NONE;
     DecodeArgs last_decode{};
+    int enc_wpc[160] = {};   // launch shape cache per (S, C)
+    int enc_ctas[160] = {};
 };
 
 namespace {
 
-cudaStream_t pick(plzgpu_ctx* c, void* s) { return s ? static_cast<cudaStream_t>(s) : c->stream; }
+// NULL selects the legacy default stream (the CUDA convention, so callers
+// passing torch's default stream handle 0 stay ordered with it).
+cudaStream_t pick(plzgpu_ctx*, void* s) { return static_cast<cudaStream_t>(s); }
 
 Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
 
 // Enqueue Kernels I-III for a device-resident input.  img must hold
 // compress_bound bytes; img_len receives the image length on the device.
 int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t n,
-                     uint8_t* img, uint64_t* d_img_len, cudaStream_t st, plzgpu_error* err) {
+                     uint8_t* img, uint64_t* d_img_len, cudaStream_t st, plzgpu_error* err,
+                     int last_stage = 3) {
     const Geometry g = geometry(n, p);
     const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
     const uint64_t G = g.n_chunks;
@@ -221,16 +226,33 @@ int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in,
         e.I = p.interval;
         e.min_match = std::max(1, p.min_match);
         e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
-        const size_t per_warp = encode_warp_smem(p.chunk_size, p.symbol_width);
-        int wpc = int(std::min<size_t>(8, std::max<size_t>(1, (200 * 1024) / per_warp)));
+        // warps per CTA that maximise resident warps per SM (smem-limited)
+        const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
+        int& wpc = c->enc_wpc[key];
+        int& per_sm = c->enc_ctas[key];
+        if (wpc == 0) {
+            int best_warps = 0;
+            for (int cand = 1; cand <= 16; ++cand) {
+                const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
+                if (ctas * cand > best_warps) {
+                    best_warps = ctas * cand;
+                    wpc = cand;
+                    per_sm = ctas;
+                }
+            }
+        }
         e.warps_per_cta = wpc;
-        int per_sm = encode_ctas_per_sm(p.symbol_width, p.chunk_size, wpc);
-        if (per_sm < 1) per_sm = 1;
         uint64_t grid = uint64_t(c->sms) * uint64_t(per_sm);
         const uint64_t need = (G + wpc - 1) / wpc;
         if (grid > need) grid = need;
         launch_encode(p.symbol_width, e, int(grid), st);
         ++launches;
+        if (last_stage == 1) {
+            CK(cudaGetLastError());
+            c->last_launches = launches;
+            c->last_op = OP_NONE;
+            return PLZGPU_OK;
+        }
         // ---- Kernel II
         ScanArgs s{};
         s.psize = e.psize;
@@ -654,6 +676,17 @@ int plzgpu_compress_async(plzgpu_ctx* c, const plzgpu_params* params, const void
                             static_cast<uint8_t*>(d_out), d_out_len, st, err);
 }
 
+int plzgpu_profile_encode(plzgpu_ctx* c, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* stream, plzgpu_error* err) {
+    clear_err(err);
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    if (n == 0) return PLZGPU_OK;
+    CK(cudaSetDevice(c->device));
+    return enqueue_compress(c, *params, static_cast<const uint8_t*>(d_in), n, nullptr, nullptr,
+                            pick(c, stream), err, 1);
+}
+
 int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, uint64_t cap,
                       uint64_t* out_len, void* stream, plzgpu_error* err) {
     clear_err(err);
@@ -753,7 +786,7 @@ int plzgpu_decompress_chunk(plzgpu_ctx* c, const void* flags, uint64_t n_flags,
     if (params->symbol_width != 1 && params->symbol_width != 2 && params->symbol_width != 4)
         return bad_field(err, "symbol_width", "{1,2,4}");
     CK(cudaSetDevice(c->device));
-    const cudaStream_t st = c->stream;
+    const cudaStream_t st = c->stream;  // private: synchronous call
     const uint64_t S = uint64_t(params->symbol_width);
     const uint64_t out_bytes = logical * S;
     // stage everything in one device scratch: flags | payload | out

@@ -252,8 +252,9 @@ std::vector<std::uint8_t> compress(std::span<const std::uint8_t> data, const Par
     std::vector<std::uint8_t> out(plzgpu_compress_bound(data.size(), &p));
     std::uint64_t len = 0;
     plzgpu_stats st{};
-    check(plzgpu_compress(detail::ctx(), &p, data.data(), data.size(), out.data(), out.size(), &len,
-                          &st, nullptr, &e),
+    plzgpu_ctx* c = detail::ctx();
+    check(plzgpu_compress(c, &p, data.data(), data.size(), out.data(), out.size(), &len, &st,
+                          plzgpu_ctx_stream(c), &e),
           e);
     out.resize(len);
     if (stats) {
@@ -289,8 +290,9 @@ std::vector<std::uint8_t> decompress_bytes(std::span<const std::uint8_t> bytes, 
     std::vector<std::uint8_t> out(plzgpu_decompressed_bound(bytes.data(), bytes.size()));
     std::uint64_t len = 0;
     plzgpu_error e;
-    check(plzgpu_decompress(detail::ctx(), bytes.data(), bytes.size(), out.data(), out.size(), &len,
-                            nullptr, &e),
+    plzgpu_ctx* c = detail::ctx();
+    check(plzgpu_decompress(c, bytes.data(), bytes.size(), out.data(), out.size(), &len,
+                            plzgpu_ctx_stream(c), &e),
           e);
     out.resize(len);
     return out;

@@ -149,5 +149,4 @@ def small_quant_codes(n_symbols: int, S: int, seed: int = 42, radius: int = None
     d = np.diff(q, prepend=0)
     radius = radius or (64 if S == 1 else 512)
     codes = np.where(np.abs(d) < radius, d + radius, 0)
-    dt = {1: np.uint8, 2: np.uint16, 4: np.uint32}[S]
-    return codes.astype(dt).astype(dt.newbyteorder("<") if hasattr(dt, "newbyteorder") else dt).tobytes()
+    return codes.astype({1: "u1", 2: "<u2", 4: "<u4"}[S]).tobytes()

@@ -213,6 +213,12 @@ class Context:
                                                C.c_void_p(d_out), cap, C.c_void_p(d_len),
                                                C.c_void_p(stream or None), C.byref(e)), e)
 
+    def encode_only(self, params: Params, d_in: int, n: int, stream: int = 0) -> None:
+        """Kernel I alone (profiling hook plzgpu_profile_encode)."""
+        e = L.Error()
+        _check(L.lib().plzgpu_profile_encode(self.handle, C.byref(params.to_c()), C.c_void_p(d_in),
+                                             n, C.c_void_p(stream or None), C.byref(e)), e)
+
     def finish(self, stream: int = 0):
         st, e = L.Stats(), L.Error()
         _check(L.lib().plzgpu_ctx_finish(self.handle, C.c_void_p(stream or None), C.byref(st),

@@ -25,7 +25,10 @@ def ref_compress(data, p):
 
 
 def ref_decompress(img):
-    return O.ref_decompress(img, 0) if O.ref_available() else O.decompress(img)
+    # threads=1: the reference rethrows the FIRST failing chunk's error, which
+    # with a thread pool is timing-dependent (parallel.hpp:36-56); one worker
+    # is its deterministic schedule (lowest chunk), which the GPU path matches
+    return O.ref_decompress(img, 1) if O.ref_available() else O.decompress(img)
 
 
 def P(S=2, W=128, C=2048, I=1, block_bytes=256 << 20):
