@@ -482,7 +482,13 @@ int plzo_decompress(const uint8_t* img, uint64_t len, uint8_t* out, uint64_t cap
     while (at < len) {
         parsed_container c;
         int rc = read_container(img + at, len - at, &c, err);
-        if (rc) return rc;
+        if (rc) {
+            if (!out) {  /* size query: the parseable prefix; errors come from decoding */
+                clear_err(err);
+                break;
+            }
+            return rc;
+        }
         if (out) {
             uint64_t k, s = (uint64_t)c.p.symbol_width, cs = c.chunk_size;
             uint64_t symbols = (c.original_len - c.tail_len) / s;
