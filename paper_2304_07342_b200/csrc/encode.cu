@@ -139,12 +139,19 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     const int C = a.C;
+    constexpr uint32_t kHead = kEncodeHeadPerS * S;  // payload bytes [0, kHead) stay here
     const size_t per_warp = encode_warp_smem(C, S);
     uint8_t* base = smem + per_warp * warp;
-    Cell* cells = reinterpret_cast<Cell*>(base);                       // C cells
-    uint8_t* pay = base + size_t(C) * sizeof(Cell);                    // C*S bytes (16B aligned)
-    uint8_t* flg = pay + size_t(C) * S;                                // C/8 bytes
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(flg + C / 8);         // 8B aligned (C/8 % 16 == 0)
+    Cell* cells = reinterpret_cast<Cell*>(base);                  // C cells (2S bytes each)
+    uint8_t* cellb = base;                                        // same bytes, byte view
+    uint8_t* raw8 = base + size_t(C) * S;                         // raw stage: upper half
+    uint8_t* head = base + size_t(C) * sizeof(Cell);              // kHead bytes
+    uint8_t* flg = head + kHead;                                  // C/8 bytes
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(flg + C / 8);    // 8B aligned
+    // Payload byte b >= kHead lands at cell byte b - kHead: it is written at
+    // a step p with b < S*(p+1), below byte 2S*(p-W) of the cell array —
+    // cells left of the window, never read again (kHead >= 2*S*W + S).
+    uint8_t* spill = cellb - kHead;
 
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
@@ -161,25 +168,34 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         const uint32_t nbytes = uint32_t(n) * S;
         const uint8_t* src = a.in + g * uint64_t(C) * S;
 
-        // ---- stage the chunk's bytes into `pay` (reused as the raw buffer)
+        // ---- stage the chunk's bytes into the upper half of the cell array
         if (a.bulk_ok && (nbytes & 15u) == 0) {
-            fence_proxy_async_smem();  // prior generic reads of `pay` before the TMA write
+            fence_proxy_async_smem();  // prior generic accesses before the TMA write
             __syncwarp();
-            if (lane == 0) bulk_g2s(pay, src, nbytes, mbar);
+            if (lane == 0) bulk_g2s(raw8, src, nbytes, mbar);
             mbar_wait(mbar, phase);
             phase ^= 1u;
         } else {
-            for (uint32_t i = lane; i < nbytes; i += 32) pay[i] = src[i];
+            for (uint32_t i = lane; i < nbytes; i += 32) raw8[i] = src[i];
             __syncwarp();
         }
 
-        // ---- packed (symbol, run) cells, right to left in 32-position words
-        const T* raw = reinterpret_cast<const T*>(pay);
+        // ---- symbols into cells, in place, left to right (a word's writes
+        // only clobber raw symbols that are already read)
+        const T* raw = reinterpret_cast<const T*>(raw8);
+        for (int w = 0; w <= (n - 1) >> 5; ++w) {
+            const int i = (w << 5) + static_cast<int>(lane);
+            const T v = i < n ? raw[i] : T(0);
+            __syncwarp();
+            if (i < n) cells[i] = Cell(v);
+            __syncwarp();
+        }
+        // ---- equal-run lengths, right to left in 32-position words
         uint32_t carry = 0;
         for (int w = (n - 1) >> 5; w >= 0; --w) {
             const int i = (w << 5) + static_cast<int>(lane);
-            const T v = i < n ? raw[i] : T(0);
-            const bool eq = (i + 1 < n) && raw[i + 1] == v;
+            const T v = i < n ? cell_sym<S>(cells[i]) : T(0);
+            const bool eq = (i + 1 < n) && cell_sym<S>(cells[i + 1]) == v;
             const uint32_t m = __ballot_sync(0xffffffffu, eq);
             const uint32_t sh = m >> lane;
             uint32_t r;
@@ -189,6 +205,7 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
                 r = static_cast<uint32_t>(__ffs(~sh));  // (#equal successors) + 1
             r = r < 255u ? r : 255u;
             carry = __shfl_sync(0xffffffffu, r, 0);
+            __syncwarp();
             if (i < n) cells[i] = make_cell<S>(v, r);
         }
         __syncwarp();
@@ -204,12 +221,13 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
             const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
             if (lane == 0) {
                 if (ptr) {
-                    pay[pl] = uint8_t(k);
-                    pay[pl + 1] = uint8_t(o);
+                    (pl < kHead ? head : spill)[pl] = uint8_t(k);
+                    (pl + 1 < kHead ? head : spill)[pl + 1] = uint8_t(o);
                 } else {
                     const T v = cell_sym<S>(cells[p]);
 #pragma unroll
-                    for (int b = 0; b < S; ++b) pay[pl + b] = uint8_t(v >> (8 * b));
+                    for (int b = 0; b < S; ++b)
+                        (pl + b < kHead ? head : spill)[pl + b] = uint8_t(v >> (8 * b));
                 }
             }
             if (ptr) fb |= 0x80u >> (t & 7u);
@@ -228,8 +246,10 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         // ---- flush to the chunk's staging slots with 128-bit stores
         const uint32_t nf = (t + 7u) >> 3;
         uint4* dp = reinterpret_cast<uint4*>(a.pay_slots + g * uint64_t(C) * S);
-        const uint4* sp = reinterpret_cast<const uint4*>(pay);
-        for (uint32_t i = lane; i < (pl + 15u) >> 4; i += 32) dp[i] = sp[i];
+        const uint32_t nv = (pl + 15u) >> 4, hv = kHead >> 4;
+        for (uint32_t i = lane; i < nv; i += 32)
+            dp[i] = i < hv ? reinterpret_cast<const uint4*>(head)[i]
+                           : reinterpret_cast<const uint4*>(cellb)[i - hv];
         uint4* df = reinterpret_cast<uint4*>(a.flag_slots + g * uint64_t(C / 8));
         const uint4* sf = reinterpret_cast<const uint4*>(flg);
         for (uint32_t i = lane; i < (nf + 15u) >> 4; i += 32) df[i] = sf[i];

@@ -31,10 +31,13 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // chunks per look-back tile
 
-// Per-warp shared-memory bytes of the encode kernel for chunk size C, width S.
+// Per-warp shared-memory bytes of the encode kernel for chunk size C, width S:
+// C (symbol, run) cells of 2S bytes (the raw chunk is staged in their upper
+// half), a kEncodeHeadPerS*S-byte payload head (the rest of the payload
+// spills into dead cells), C/8 flag bytes and an mbarrier.
+constexpr uint32_t kEncodeHeadPerS = 512;  // >= 2*W + 1 for W <= 255
 __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
-    const size_t cell = S == 1 ? 2 : (S == 2 ? 4 : 8);
-    size_t b = size_t(C) * cell + size_t(C) * S + size_t(C) / 8 + 16;
+    size_t b = size_t(C) * 2 * S + size_t(kEncodeHeadPerS) * S + size_t(C) / 8 + 16;
     return (b + 15) & ~size_t(15);
 }
 
