@@ -100,6 +100,82 @@ __device__ __forceinline__ void eval_window(const typename Sym<S>::Cell* __restr
                                 best, pending);
 }
 
+// ---- S in {1, 2}: two adjacent candidates per lane-instruction ------------
+// Candidates are taken in aligned pairs (w, w+1), w even, so one shared load
+// fetches both cells; symbols and runs are split into 16-bit halves with PRMT
+// and evaluated with native 16x2 SIMD min/max (VIMNMX.U16x2).  Keys are the
+// same (len << 8 | off) as the scalar path, one per half.
+__device__ __forceinline__ uint32_t vmin2(uint32_t a, uint32_t b) { return __vminu2(a, b); }
+__device__ __forceinline__ uint32_t vmax2(uint32_t a, uint32_t b) { return __vmaxu2(a, b); }
+
+template <int S>
+__device__ __forceinline__ void load_pair(const typename Sym<S>::Cell* cells, int w,
+                                          uint32_t& sym2, uint32_t& run2) {
+    if constexpr (S == 1) {  // cell = sym8 | run8 << 8; a pair is one u32
+        const uint32_t c = *reinterpret_cast<const uint32_t*>(cells + w);
+        sym2 = __byte_perm(c, 0u, 0x4240);
+        run2 = __byte_perm(c, 0u, 0x4341);
+    } else {  // cell = sym16 | run8 << 16; a pair is one u64
+        const uint2 c = *reinterpret_cast<const uint2*>(cells + w);
+        sym2 = __byte_perm(c.x, c.y, 0x5410);
+        run2 = __byte_perm(c.x, c.y, 0x7632);  // bytes 3/7 of a cell are zero
+    }
+}
+
+template <int S, bool kCap, bool kMask>
+__device__ __forceinline__ void eval_pair(const typename Sym<S>::Cell* cells, int w, int oa,
+                                          int lim, uint32_t s2, uint32_t rp2, uint32_t cap2,
+                                          uint32_t bit, uint32_t& best2, uint32_t& pending) {
+    uint32_t sym2, run2;
+    load_pair<S>(cells, w, sym2, run2);
+    uint32_t o2 = (uint32_t(oa) & 0xffffu) | (uint32_t(oa - 1) << 16);
+    // halves outside the window may hold offsets >= 256 (or wrapped negatives):
+    // clamp so len * 256 + off cannot carry into the neighbouring half
+    if constexpr (kMask) o2 = vmin2(o2, 0x00ff00ffu);
+    const uint32_t ub2 = kCap ? vmin2(o2, cap2) : o2;
+    const uint32_t d = sym2 ^ s2;
+    const uint32_t differ = vmin2(d, 0x00010001u);                 // 1 where symbols differ
+    const uint32_t keep = (differ ^ 0x00010001u) * 0xffffu;        // 0xffff where equal
+    const uint32_t k2 = vmin2(vmin2(run2, rp2), ub2) & keep;       // same symbol: shorter run
+    uint32_t key2 = k2 * 256u + o2;
+    uint32_t ident = vmin2(d | (run2 ^ rp2), 0x00010001u) ^ 0x00010001u;  // identical cells
+    if constexpr (kMask) {  // halves with offset outside [1, lim]
+        const uint32_t m = ((oa >= 1 && oa <= lim) ? 0x0000ffffu : 0u) |
+                           ((oa - 1 >= 1 && oa - 1 <= lim) ? 0xffff0000u : 0u);
+        key2 &= m;
+        ident &= m;
+    }
+    best2 = vmax2(best2, key2);
+    pending += ident * bit;  // bits r (half a) and 16 + r (half b)
+}
+
+template <int S, bool kCap>
+__device__ __forceinline__ uint32_t pair_window(const typename Sym<S>::Cell* __restrict__ cells,
+                                                int p, int lim, uint32_t cap, uint32_t s2,
+                                                uint32_t rp2, uint32_t lane, uint32_t& pending,
+                                                int& w0_out) {
+    const int w0 = (p - lim) & ~1;                 // pairs cover [w0, w0 + 2*npairs) >= window
+    const int npairs = (p - w0 + 1) >> 1;
+    const uint32_t cap2 = cap * 0x00010001u;
+    const int wl = w0 + 2 * static_cast<int>(lane);
+    const int oa0 = p - wl;
+    uint32_t best2 = 0;
+    if (npairs == 128) {  // W = 255 steady state: 4 rounds, edges only in rounds 0 and 3
+        eval_pair<S, kCap, true>(cells, wl, oa0, lim, s2, rp2, cap2, 1u, best2, pending);
+        eval_pair<S, kCap, false>(cells, wl + 64, oa0 - 64, lim, s2, rp2, cap2, 2u, best2, pending);
+        eval_pair<S, kCap, false>(cells, wl + 128, oa0 - 128, lim, s2, rp2, cap2, 4u, best2, pending);
+        eval_pair<S, kCap, true>(cells, wl + 192, oa0 - 192, lim, s2, rp2, cap2, 8u, best2, pending);
+    } else {
+        const int rounds = (npairs + 31) >> 5;
+        for (int r = 0; r < rounds; ++r)
+            eval_pair<S, kCap, true>(cells, wl + 64 * r, oa0 - 64 * r, lim, s2, rp2, cap2, 1u << r,
+                                     best2, pending);
+    }
+    w0_out = w0;
+    const uint32_t lo = best2 & 0xffffu, hi = best2 >> 16;
+    return lo > hi ? lo : hi;
+}
+
 template <int S>
 __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell* __restrict__ cells,
                                                     int p, int n, int W, uint32_t lane) {
@@ -112,12 +188,41 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
     const Cell* cw = cells + (p - o0);              // round r: cw[32r]
     const int full = lim >> 5;                      // rounds where every lane is valid
     uint32_t best = 0, pending = 0;
-    if (cap == 255)
+    if constexpr (S <= 2) {
+        int w0 = 0;
+        const uint32_t s2 = uint32_t(cell_sym<S>(cp)) * 0x00010001u, rp2 = rp * 0x00010001u;
+        best = cap == 255 ? pair_window<S, false>(cells, p, lim, cap, s2, rp2, lane, pending, w0)
+                          : pair_window<S, true>(cells, p, lim, cap, s2, rp2, lane, pending, w0);
+        if (__any_sync(0xffffffffu, pending != 0)) {
+            while (pending) {
+                const int b = __ffs(pending) - 1;
+                pending &= pending - 1;
+                const int w = w0 + 2 * (static_cast<int>(lane) + 32 * (b & 15)) + (b >> 4);
+                const int o = p - w;
+                const int ub = o < int(cap) ? o : int(cap);
+                if (int(rp) >= ub) continue;
+                const uint32_t k = uint32_t(lcp_continue<S>(cells, w, p, static_cast<int>(rp), ub));
+                const uint32_t key = (k << 8) | uint32_t(o);
+                best = key > best ? key : best;
+            }
+        }
+        return __reduce_max_sync(0xffffffffu, best);
+    }
+    if (cap == 255 && full == 7) {  // steady state of W = 255: straight-line 7 rounds + tail
+#pragma unroll
+        for (int r = 0; r < 7; ++r)
+            eval_candidate<S, false>(cw[32 * r], cp, rp, uint32_t(o0 - 32 * r), cap, 1u << r, best,
+                                     pending);
+        if (o0 - 224 >= 1)
+            eval_candidate<S, false>(cw[224], cp, rp, uint32_t(o0 - 224), cap, 1u << 7, best,
+                                     pending);
+    } else if (cap == 255) {
         eval_window<S, false>(cw, cp, rp, o0, full, cap, best, pending);
-    else
+    } else {
         eval_window<S, true>(cw, cp, rp, o0, full, cap, best, pending);
+    }
     // identical cells: both runs end together, continue at relative rp
-    while (pending) {
+    if (__any_sync(0xffffffffu, pending != 0)) while (pending) {
         const int r = __ffs(pending) - 1;
         pending &= pending - 1;
         const int o = o0 - 32 * r;
@@ -142,16 +247,16 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     constexpr uint32_t kHead = kEncodeHeadPerS * S;  // payload bytes [0, kHead) stay here
     const size_t per_warp = encode_warp_smem(C, S);
     uint8_t* base = smem + per_warp * warp;
-    Cell* cells = reinterpret_cast<Cell*>(base);                  // C cells (2S bytes each)
-    uint8_t* cellb = base;                                        // same bytes, byte view
-    uint8_t* raw8 = base + size_t(C) * S;                         // raw stage: upper half
-    uint8_t* head = base + size_t(C) * sizeof(Cell);              // kHead bytes
-    uint8_t* flg = head + kHead;                                  // C/8 bytes
+    // [payload head: kHead B][cells: C x 2S B][flags: C/8 B][mbarrier]
+    // Payload byte b is stored at head[b]: beyond kHead it runs on into the
+    // cell array, at cell byte b - kHead.  It is written at a step p with
+    // b < S*(p+1) <= kHead + 2S*(p-W), i.e. over cells left of the window that
+    // are never read again (kHead >= 2*S*W + S).
+    uint8_t* head = base;
+    Cell* cells = reinterpret_cast<Cell*>(base + kHead);          // C cells (2S bytes each)
+    uint8_t* raw8 = base + kHead + size_t(C) * S;                 // raw stage: upper half
+    uint8_t* flg = base + kHead + size_t(C) * sizeof(Cell);       // C/8 bytes
     uint64_t* mbar = reinterpret_cast<uint64_t*>(flg + C / 8);    // 8B aligned
-    // Payload byte b >= kHead lands at cell byte b - kHead: it is written at
-    // a step p with b < S*(p+1), below byte 2S*(p-W) of the cell array —
-    // cells left of the window, never read again (kHead >= 2*S*W + S).
-    uint8_t* spill = cellb - kHead;
 
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
@@ -221,13 +326,12 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
             const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
             if (lane == 0) {
                 if (ptr) {
-                    (pl < kHead ? head : spill)[pl] = uint8_t(k);
-                    (pl + 1 < kHead ? head : spill)[pl + 1] = uint8_t(o);
+                    head[pl] = uint8_t(k);
+                    head[pl + 1] = uint8_t(o);
                 } else {
                     const T v = cell_sym<S>(cells[p]);
 #pragma unroll
-                    for (int b = 0; b < S; ++b)
-                        (pl + b < kHead ? head : spill)[pl + b] = uint8_t(v >> (8 * b));
+                    for (int b = 0; b < S; ++b) head[pl + b] = uint8_t(v >> (8 * b));
                 }
             }
             if (ptr) fb |= 0x80u >> (t & 7u);
@@ -246,10 +350,8 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         // ---- flush to the chunk's staging slots with 128-bit stores
         const uint32_t nf = (t + 7u) >> 3;
         uint4* dp = reinterpret_cast<uint4*>(a.pay_slots + g * uint64_t(C) * S);
-        const uint32_t nv = (pl + 15u) >> 4, hv = kHead >> 4;
-        for (uint32_t i = lane; i < nv; i += 32)
-            dp[i] = i < hv ? reinterpret_cast<const uint4*>(head)[i]
-                           : reinterpret_cast<const uint4*>(cellb)[i - hv];
+        const uint4* sp = reinterpret_cast<const uint4*>(head);
+        for (uint32_t i = lane; i < (pl + 15u) >> 4; i += 32) dp[i] = sp[i];
         uint4* df = reinterpret_cast<uint4*>(a.flag_slots + g * uint64_t(C / 8));
         const uint4* sf = reinterpret_cast<const uint4*>(flg);
         for (uint32_t i = lane; i < (nf + 15u) >> 4; i += 32) df[i] = sf[i];

@@ -37,7 +37,9 @@ constexpr int kScanTile = kScanThreads * kScanItems;  // chunks per look-back ti
 // spills into dead cells), C/8 flag bytes and an mbarrier.
 constexpr uint32_t kEncodeHeadPerS = 512;  // >= 2*W + 1 for W <= 255
 __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
-    size_t b = size_t(C) * 2 * S + size_t(kEncodeHeadPerS) * S + size_t(C) / 8 + 16;
+    // + 64 cells of slack: the last partial round of pair candidates may read
+    // (and discard) up to 62 cells past the chunk end
+    size_t b = size_t(C) * 2 * S + size_t(kEncodeHeadPerS) * S + size_t(C) / 8 + 16 + 128 * S;
     return (b + 15) & ~size_t(15);
 }
 
