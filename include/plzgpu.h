@@ -164,6 +164,51 @@ int plzgpu_decompress_chunk(plzgpu_ctx* ctx, const void* flags, uint64_t n_flags
                             const plzgpu_params* params, uint64_t chunk_index, void* out,
                             plzgpu_error* err);
 
+/* ---------------------------------------------------- multi-GPU shards */
+/* SURVEY.md §8e.  Chunks are independent, so any contiguous chunk range of
+ * the input's partition compresses on its own GPU; ranks then agree on
+ * per-container stream totals (a few u64 over NCCL), each writes the table
+ * and stream slices it owns as image segments, and the root gathers them and
+ * writes the container headers.  The gathered image equals plzgpu_compress of
+ * the whole input, byte for byte. */
+
+/* chunk / container counts of the partition of n input bytes */
+uint64_t plzgpu_num_chunks(uint64_t n, const plzgpu_params* params);
+uint64_t plzgpu_num_containers(uint64_t n, const plzgpu_params* params);
+
+/* Kernels I+II over chunks [chunk_begin, chunk_end) of an n_total-byte input.
+ * `in` (host or device) points at byte chunk_begin*C*S of the input and
+ * holds the range's bytes (for the final range: through the end of the
+ * input, tail included).  totals receives, per container the range touches
+ * (in order), {container index, payload bytes, flag bytes}.  The context keeps
+ * the encoded range for plzgpu_shard_assemble. */
+int plzgpu_shard_encode(plzgpu_ctx* ctx, const plzgpu_params* params, const void* in,
+                        uint64_t n_total, uint64_t chunk_begin, uint64_t chunk_end,
+                        uint64_t* totals, uint64_t max_touched, uint64_t* n_touched, void* stream,
+                        plzgpu_error* err);
+
+/* Host arithmetic: the image segments {image_offset, local_offset, length}
+ * (4 per touched container: payload-table slice, flag-table slice, flag
+ * bytes, payload bytes) of a shard, given its totals and, per touched
+ * container, bases = {payload_base, flag_base, container image offset,
+ * container flag total}.  Returns the segment count. */
+uint64_t plzgpu_shard_segments(const plzgpu_params* params, uint64_t n_total, uint64_t chunk_begin,
+                               uint64_t chunk_end, const uint64_t* totals, const uint64_t* bases,
+                               uint64_t n_touched, uint64_t* segs, uint64_t max_segs);
+
+/* Write the last plzgpu_shard_encode's segments into d_out (device), laid
+ * out back to back in segment order; segs as plzgpu_shard_segments. */
+int plzgpu_shard_assemble(plzgpu_ctx* ctx, const uint64_t* bases, void* d_out, uint64_t cap,
+                          uint64_t* segs, uint64_t max_segs, uint64_t* n_segs, uint64_t* out_len,
+                          void* stream, plzgpu_error* err);
+
+/* Root: write every container's header, final table entries and tail into
+ * d_img given per-container {payload total, flag total} for ALL containers and
+ * the input's last tail_len (< S) bytes (host).  *img_len = image length. */
+int plzgpu_shard_headers(plzgpu_ctx* ctx, const plzgpu_params* params, uint64_t n_total,
+                         const uint64_t* totals, const void* tail, void* d_img, uint64_t cap,
+                         uint64_t* img_len, void* stream, plzgpu_error* err);
+
 /* ------------------------------------------------------ profiling hook */
 
 /* Enqueue Kernel I (match + encode) alone on a device input, so its share of

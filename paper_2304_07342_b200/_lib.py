@@ -74,6 +74,16 @@ SIGNATURES = [
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),
     ("plzgpu_decompress_chunk", C.c_int, [_VP, _VP, _U64, _VP, _U64, _U64, _P, _U64, _VP, _E]),
     ("plzgpu_profile_encode", C.c_int, [_VP, _P, _VP, _U64, _VP, _E]),
+    ("plzgpu_num_chunks", _U64, [_U64, _P]),
+    ("plzgpu_num_containers", _U64, [_U64, _P]),
+    ("plzgpu_shard_encode", C.c_int, [_VP, _P, _VP, _U64, _U64, _U64, C.POINTER(_U64), _U64,
+                                      C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_shard_segments", _U64, [_P, _U64, _U64, _U64, C.POINTER(_U64), C.POINTER(_U64), _U64,
+                                     C.POINTER(_U64), _U64]),
+    ("plzgpu_shard_assemble", C.c_int, [_VP, C.POINTER(_U64), _VP, _U64, C.POINTER(_U64), _U64,
+                                        C.POINTER(_U64), C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_shard_headers", C.c_int, [_VP, _P, _U64, C.POINTER(_U64), _VP, _VP, _U64,
+                                       C.POINTER(_U64), _VP, _E]),
 ]
 
 _lib = None

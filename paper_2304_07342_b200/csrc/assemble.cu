@@ -91,7 +91,71 @@ __global__ void plz_headers_kernel(AssembleArgs a) {
     if (j + 1 == a.n_blocks) *a.img_len = img0 + 26 + 8 * (n + 1) + ftot + ptot + tail;
 }
 
+// Shard variant of Kernel III (multi-GPU): the same per-chunk
+// copies into a local segment buffer with offsets rebased by the shard's
+// position inside each container's streams.
+__global__ void __launch_bounds__(256) plz_shard_assemble_kernel(ShardAssembleArgs a) {
+    const uint32_t lane = lane_id();
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
+    for (uint64_t g = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         g < a.n_chunks; g += warps) {
+        uint64_t c = 0;
+        while (c + 1 < a.n_conts && a.conts[c + 1].g_lo <= g) ++c;
+        const ShardCont& d = a.conts[c];
+        const uint64_t i = g - d.g_lo;
+        const uint64_t lp = a.P64[g] - a.P64[d.g_lo], lf = a.F64[g] - a.F64[d.g_lo];
+        const uint64_t pk = d.p_base + lp, fk = d.f_base + lf;
+        if (lane == 0 && (pk > 0xffffffffull || fk > 0xffffffffull)) atomicExch(a.overflow, 1u);
+        if (lane < 4) {
+            a.out[d.seg_ptab + 4 * i + lane] = uint8_t(pk >> (8 * lane));
+        } else if (lane < 8) {
+            a.out[d.seg_ftab + 4 * i + (lane - 4)] = uint8_t(fk >> (8 * (lane - 4)));
+        }
+        warp_copy_realign(a.out + d.seg_flags + lf, a.flag_slots + g * (C / 8), a.fsize[g], lane);
+        warp_copy_realign(a.out + d.seg_pay + lp, a.pay_slots + g * C * S, a.psize[g], lane);
+    }
+}
+
+__global__ void plz_shard_headers_kernel(const HeaderDesc* descs, uint64_t n_conts, uint8_t* img,
+                                         int S, int W, int I, int C) {
+    const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n_conts) return;
+    const HeaderDesc d = descs[j];
+    uint8_t* h = img + d.img_off;
+    h[0] = 'P'; h[1] = 'L'; h[2] = 'Z'; h[3] = '1';
+    h[4] = 1;
+    h[5] = uint8_t(S);
+    h[6] = uint8_t(W);
+    h[7] = uint8_t(I);
+    h[8] = 0;
+    st_le32(h + 9, uint32_t(C));
+    st_le32(h + 13, uint32_t(d.byte_len));
+    st_le32(h + 17, uint32_t(d.byte_len >> 32));
+    st_le32(h + 21, d.n);
+    h[25] = d.tail_len;
+    const uint64_t n = d.n;
+    st_le32(h + 26 + 4 * n, uint32_t(d.ptot));
+    st_le32(h + 26 + 4 * (n + 1) + 4 * n, uint32_t(d.ftot));
+    uint8_t* t = h + 26 + 8 * (n + 1) + d.ftot + d.ptot;
+    for (uint32_t i = 0; i < d.tail_len; ++i) t[i] = d.tail[i];
+}
+
 }  // namespace
+
+void launch_shard_assemble(const ShardAssembleArgs& a, cudaStream_t st) {
+    if (a.n_chunks == 0) return;
+    uint64_t blocks = (a.n_chunks + 7) / 8;
+    if (blocks > 148ull * 16) blocks = 148ull * 16;
+    plz_shard_assemble_kernel<<<unsigned(blocks), 256, 0, st>>>(a);
+}
+
+void launch_shard_headers(const HeaderDesc* d, uint64_t n_conts, uint8_t* img, int S, int W, int I,
+                          int C, cudaStream_t st) {
+    if (n_conts == 0) return;
+    plz_shard_headers_kernel<<<unsigned((n_conts + 127) / 128), 128, 0, st>>>(d, n_conts, img, S, W,
+                                                                              I, C);
+}
 
 void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     if (a.n_chunks == 0) return;

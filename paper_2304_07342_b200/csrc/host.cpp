@@ -17,6 +17,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "../../include/plzgpu.h"
 #include "kernels.h"
@@ -176,6 +177,11 @@ struct plzgpu_ctx {
     DecodeArgs last_decode{};
     int enc_wpc[160] = {};   // launch shape cache per (S, C)
     int enc_ctas[160] = {};
+    DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
+    // last plzgpu_shard_encode: the range and its per-container local totals
+    uint64_t sh_begin = 0, sh_end = 0, sh_n = 0;
+    plzgpu_params sh_params{};
+    std::vector<uint64_t> sh_touch;  // per touched container: {j, lo, hi, P, F}
 };
 
 namespace {
@@ -188,12 +194,13 @@ Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
 
 // Enqueue Kernels I-III for a device-resident input.  img must hold
 // compress_bound bytes; img_len receives the image length on the device.
-int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t n,
-                     uint8_t* img, uint64_t* d_img_len, cudaStream_t st, plzgpu_error* err,
-                     int last_stage = 3) {
-    const Geometry g = geometry(n, p);
+// Kernels I and II over G chunks starting at d_in (chunk g at g*C*S); the
+// last of them has logical length last_len.  Leaves psize/fsize, staging
+// slots and exclusive prefixes P64/F64[0..G] in the context.
+int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t G,
+                        uint32_t last_len, cudaStream_t st, plzgpu_error* err, int* launches,
+                        bool scan = true) {
     const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
-    const uint64_t G = g.n_chunks;
     const uint64_t tiles = (G + kScanTile - 1) / kScanTile;
     CK(c->pay_slots.ensure(G * C * S + 64));
     CK(c->flag_slots.ensure(G * (C / 8) + 64));
@@ -207,69 +214,83 @@ int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in,
     Meta* m = dmeta(c);
     CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
     CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
-    int launches = 0;
-    if (G > 0) {
-        CK(cudaMemsetAsync(c->status.p, 0, tiles * 4, st));
-        // ---- Kernel I
-        EncodeArgs e{};
-        e.in = d_in;
-        e.pay_slots = c->pay_slots.as<uint8_t>();
-        e.flag_slots = c->flag_slots.as<uint8_t>();
-        e.psize = c->psize.as<uint32_t>();
-        e.fsize = c->fsize.as<uint32_t>();
-        e.stats = m->stats;
-        e.work = &m->work[0];
-        e.n_chunks = G;
-        e.last_len = g.last_len;
-        e.C = p.chunk_size;
-        e.W = p.window;
-        e.I = p.interval;
-        e.min_match = std::max(1, p.min_match);
-        e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
-        // warps per CTA that maximise resident warps per SM (smem-limited)
-        const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
-        int& wpc = c->enc_wpc[key];
-        int& per_sm = c->enc_ctas[key];
-        if (wpc == 0) {
-            int best_warps = 0;
-            for (int cand = 1; cand <= 16; ++cand) {
-                const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
-                if (ctas * cand > best_warps) {
-                    best_warps = ctas * cand;
-                    wpc = cand;
-                    per_sm = ctas;
-                }
-            }
-        }
-        e.warps_per_cta = wpc;
-        uint64_t grid = uint64_t(c->sms) * uint64_t(per_sm);
-        const uint64_t need = (G + wpc - 1) / wpc;
-        if (grid > need) grid = need;
-        launch_encode(p.symbol_width, e, int(grid), st);
-        ++launches;
-        if (last_stage == 1) {
-            CK(cudaGetLastError());
-            c->last_launches = launches;
-            c->last_op = OP_NONE;
-            return PLZGPU_OK;
-        }
-        // ---- Kernel II
-        ScanArgs s{};
-        s.psize = e.psize;
-        s.fsize = e.fsize;
-        s.n = G;
-        s.P64 = c->p64.as<uint64_t>();
-        s.F64 = c->f64.as<uint64_t>();
-        s.status = c->status.as<uint32_t>();
-        s.agg = c->agg.as<ulonglong2>();
-        s.incl = c->incl.as<ulonglong2>();
-        s.tile_counter = &m->work[1];
-        launch_scan(s, st);
-        ++launches;
-    } else {
+    if (G == 0) {
         CK(cudaMemsetAsync(c->p64.p, 0, 8, st));
         CK(cudaMemsetAsync(c->f64.p, 0, 8, st));
+        return PLZGPU_OK;
     }
+    CK(cudaMemsetAsync(c->status.p, 0, tiles * 4, st));
+    // ---- Kernel I
+    EncodeArgs e{};
+    e.in = d_in;
+    e.pay_slots = c->pay_slots.as<uint8_t>();
+    e.flag_slots = c->flag_slots.as<uint8_t>();
+    e.psize = c->psize.as<uint32_t>();
+    e.fsize = c->fsize.as<uint32_t>();
+    e.stats = m->stats;
+    e.work = &m->work[0];
+    e.n_chunks = G;
+    e.last_len = last_len;
+    e.C = p.chunk_size;
+    e.W = p.window;
+    e.I = p.interval;
+    e.min_match = std::max(1, p.min_match);
+    e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
+    // warps per CTA that maximise resident warps per SM (smem-limited)
+    const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
+    int& wpc = c->enc_wpc[key];
+    int& per_sm = c->enc_ctas[key];
+    if (wpc == 0) {
+        int best_warps = 0;
+        for (int cand = 1; cand <= 16; ++cand) {
+            const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
+            if (ctas * cand > best_warps) {
+                best_warps = ctas * cand;
+                wpc = cand;
+                per_sm = ctas;
+            }
+        }
+    }
+    e.warps_per_cta = wpc;
+    uint64_t grid = uint64_t(c->sms) * uint64_t(per_sm);
+    const uint64_t need = (G + wpc - 1) / wpc;
+    if (grid > need) grid = need;
+    launch_encode(p.symbol_width, e, int(grid), st);
+    ++*launches;
+    if (!scan) return PLZGPU_OK;
+    // ---- Kernel II
+    ScanArgs sa{};
+    sa.psize = e.psize;
+    sa.fsize = e.fsize;
+    sa.n = G;
+    sa.P64 = c->p64.as<uint64_t>();
+    sa.F64 = c->f64.as<uint64_t>();
+    sa.status = c->status.as<uint32_t>();
+    sa.agg = c->agg.as<ulonglong2>();
+    sa.incl = c->incl.as<ulonglong2>();
+    sa.tile_counter = &m->work[1];
+    launch_scan(sa, st);
+    ++*launches;
+    return PLZGPU_OK;
+}
+
+// Enqueue Kernels I-III for a device-resident input.  img must hold
+// compress_bound bytes; img_len receives the image length on the device.
+int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t n,
+                     uint8_t* img, uint64_t* d_img_len, cudaStream_t st, plzgpu_error* err,
+                     int last_stage = 3) {
+    const Geometry g = geometry(n, p);
+    const uint64_t G = g.n_chunks;
+    int launches = 0;
+    int rc = enqueue_encode_scan(c, p, d_in, G, g.last_len, st, err, &launches, last_stage > 1);
+    if (rc) return rc;
+    if (last_stage == 1) {
+        CK(cudaGetLastError());
+        c->last_launches = launches;
+        c->last_op = OP_NONE;
+        return PLZGPU_OK;
+    }
+    Meta* m = dmeta(c);
     // ---- Kernel III + headers
     AssembleArgs a{};
     a.in = d_in;
@@ -824,6 +845,235 @@ int plzgpu_decompress_chunk(plzgpu_ctx* c, const void* flags, uint64_t n_flags,
                            is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                            st));
     CK(cudaStreamSynchronize(st));
+    return PLZGPU_OK;
+}
+
+// ------------------------------------------------------------ shards
+
+// Segments of the final image a shard owns in one container:
+// its slice of each offset table and of both streams.  Pure host arithmetic.
+static uint64_t shard_segments_impl(const plzgpu_params& p, uint64_t n_total, uint64_t begin,
+                                    uint64_t end, const uint64_t* totals, const uint64_t* bases,
+                                    uint64_t n_touched, uint64_t* segs, uint64_t max_segs) {
+    const Geometry g = geometry(n_total, p);
+    uint64_t count = 0, local = 0;
+    for (uint64_t i = 0; i < n_touched; ++i) {
+        const uint64_t j = totals[3 * i];
+        const uint64_t g0 = j * g.cpb;
+        const uint64_t nj = (j + 1 == g.n_blocks) ? g.n_chunks - g0 : g.cpb;
+        const uint64_t lo = std::max(begin, g0), hi = std::min(end, g0 + nj);
+        const uint64_t k_lo = lo - g0, cnt = hi - lo;
+        const uint64_t lp = totals[3 * i + 1], lf = totals[3 * i + 2];
+        const uint64_t p_base = bases[4 * i], f_base = bases[4 * i + 1];
+        const uint64_t img_off = bases[4 * i + 2], f_total = bases[4 * i + 3];
+        const uint64_t tabs = img_off + 26, streams = tabs + 8 * (nj + 1);
+        const uint64_t seg[4][2] = {{tabs + 4 * k_lo, 4 * cnt},
+                                    {tabs + 4 * (nj + 1) + 4 * k_lo, 4 * cnt},
+                                    {streams + f_base, lf},
+                                    {streams + f_total + p_base, lp}};
+        for (const auto& sg : seg) {
+            if (count < max_segs && segs) {
+                segs[3 * count] = sg[0];
+                segs[3 * count + 1] = local;
+                segs[3 * count + 2] = sg[1];
+            }
+            local += sg[1];
+            ++count;
+        }
+    }
+    return count;
+}
+
+uint64_t plzgpu_num_chunks(uint64_t n, const plzgpu_params* p) { return geometry(n, *p).n_chunks; }
+
+uint64_t plzgpu_num_containers(uint64_t n, const plzgpu_params* p) {
+    return geometry(n, *p).n_blocks;
+}
+
+uint64_t plzgpu_shard_segments(const plzgpu_params* p, uint64_t n_total, uint64_t chunk_begin,
+                               uint64_t chunk_end, const uint64_t* totals, const uint64_t* bases,
+                               uint64_t n_touched, uint64_t* segs, uint64_t max_segs) {
+    return shard_segments_impl(*p, n_total, chunk_begin, chunk_end, totals, bases, n_touched, segs,
+                               max_segs);
+}
+
+int plzgpu_shard_encode(plzgpu_ctx* c, const plzgpu_params* params, const void* in,
+                        uint64_t n_total, uint64_t chunk_begin, uint64_t chunk_end,
+                        uint64_t* totals, uint64_t max_touched, uint64_t* n_touched, void* stream,
+                        plzgpu_error* err) {
+    clear_err(err);
+    *n_touched = 0;
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    const plzgpu_params& p = *params;
+    const Geometry g = geometry(n_total, p);
+    if (chunk_begin > chunk_end || chunk_end > g.n_chunks)
+        return set_err(err, PLZGPU_CONTRACT, 0, kNoIndex, kNoIndex, "shard range outside the input");
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
+    const uint64_t L = chunk_end - chunk_begin;
+    const uint32_t last_len = chunk_end == g.n_chunks ? g.last_len : uint32_t(C);
+    uint64_t local_bytes = L * C * S;
+    if (chunk_end == g.n_chunks && L) local_bytes = n_total - chunk_begin * C * S;
+    const uint8_t* d_in = static_cast<const uint8_t*>(in);
+    if (L && !is_device_ptr(in)) {
+        CK(c->in.ensure(local_bytes + 16));
+        CK(cudaMemcpyAsync(c->in.p, in, local_bytes, cudaMemcpyHostToDevice, st));
+        d_in = c->in.as<uint8_t>();
+    }
+    int launches = 0;
+    rc = enqueue_encode_scan(c, p, d_in, L, last_len, st, err, &launches);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    c->last_launches = launches;
+    // per touched container: local prefix values at its range ends
+    c->sh_touch.clear();
+    const uint64_t j_first = L ? chunk_begin / g.cpb : 0, j_last = L ? (chunk_end - 1) / g.cpb : 0;
+    std::vector<uint64_t> idx;
+    for (uint64_t j = j_first; L && j <= j_last; ++j) {
+        const uint64_t lo = std::max(chunk_begin, j * g.cpb);
+        const uint64_t hi = std::min(chunk_end, std::min((j + 1) * g.cpb, g.n_chunks));
+        c->sh_touch.insert(c->sh_touch.end(), {j, lo, hi, 0, 0});
+        idx.push_back(lo - chunk_begin);
+        idx.push_back(hi - chunk_begin);
+    }
+    std::vector<uint64_t> pv(idx.size()), fv(idx.size());
+    for (size_t i = 0; i < idx.size(); ++i) {
+        CK(cudaMemcpyAsync(&pv[i], c->p64.as<uint64_t>() + idx[i], 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&fv[i], c->f64.as<uint64_t>() + idx[i], 8, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    const uint64_t nt = c->sh_touch.size() / 5;
+    for (uint64_t i = 0; i < nt; ++i) {
+        c->sh_touch[5 * i + 3] = pv[2 * i + 1] - pv[2 * i];
+        c->sh_touch[5 * i + 4] = fv[2 * i + 1] - fv[2 * i];
+        if (i < max_touched && totals) {
+            totals[3 * i] = c->sh_touch[5 * i];
+            totals[3 * i + 1] = c->sh_touch[5 * i + 3];
+            totals[3 * i + 2] = c->sh_touch[5 * i + 4];
+        }
+    }
+    c->sh_begin = chunk_begin;
+    c->sh_end = chunk_end;
+    c->sh_n = n_total;
+    c->sh_params = p;
+    *n_touched = nt;
+    return PLZGPU_OK;
+}
+
+int plzgpu_shard_assemble(plzgpu_ctx* c, const uint64_t* bases, void* d_out, uint64_t cap,
+                          uint64_t* segs, uint64_t max_segs, uint64_t* n_segs, uint64_t* out_len,
+                          void* stream, plzgpu_error* err) {
+    clear_err(err);
+    *n_segs = 0;
+    *out_len = 0;
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const plzgpu_params& p = c->sh_params;
+    const uint64_t nt = c->sh_touch.size() / 5;
+    std::vector<uint64_t> totals(3 * nt);
+    for (uint64_t i = 0; i < nt; ++i) {
+        totals[3 * i] = c->sh_touch[5 * i];
+        totals[3 * i + 1] = c->sh_touch[5 * i + 3];
+        totals[3 * i + 2] = c->sh_touch[5 * i + 4];
+    }
+    std::vector<uint64_t> sg(12 * nt + 3);
+    const uint64_t ns = shard_segments_impl(p, c->sh_n, c->sh_begin, c->sh_end, totals.data(), bases,
+                                            nt, sg.data(), 4 * nt);
+    uint64_t total = 0;
+    for (uint64_t i = 0; i < ns; ++i) total += sg[3 * i + 2];
+    if (total > cap)
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex, "shard buffer too small");
+    std::vector<ShardCont> conts(nt);
+    for (uint64_t i = 0; i < nt; ++i) {
+        const Geometry g = geometry(c->sh_n, p);
+        ShardCont& d = conts[i];
+        const uint64_t j = c->sh_touch[5 * i], lo = c->sh_touch[5 * i + 1];
+        d.g_lo = lo - c->sh_begin;
+        d.g_hi = c->sh_touch[5 * i + 2] - c->sh_begin;
+        d.k_lo = lo - j * g.cpb;
+        d.p_base = bases[4 * i];
+        d.f_base = bases[4 * i + 1];
+        d.seg_ptab = sg[3 * (4 * i) + 1];
+        d.seg_ftab = sg[3 * (4 * i + 1) + 1];
+        d.seg_flags = sg[3 * (4 * i + 2) + 1];
+        d.seg_pay = sg[3 * (4 * i + 3) + 1];
+    }
+    if (nt) {
+        CK(c->shard_desc.ensure(nt * sizeof(ShardCont)));
+        CK(cudaMemcpyAsync(c->shard_desc.p, conts.data(), nt * sizeof(ShardCont),
+                           cudaMemcpyHostToDevice, st));
+        Meta* m = dmeta(c);
+        CK(cudaMemsetAsync(&m->overflow, 0, sizeof m->overflow, st));
+        ShardAssembleArgs a{};
+        a.pay_slots = c->pay_slots.as<uint8_t>();
+        a.flag_slots = c->flag_slots.as<uint8_t>();
+        a.psize = c->psize.as<uint32_t>();
+        a.fsize = c->fsize.as<uint32_t>();
+        a.P64 = c->p64.as<uint64_t>();
+        a.F64 = c->f64.as<uint64_t>();
+        a.conts = c->shard_desc.as<ShardCont>();
+        a.n_conts = nt;
+        a.out = static_cast<uint8_t*>(d_out);
+        a.overflow = &m->overflow;
+        a.n_chunks = c->sh_end - c->sh_begin;
+        a.S = p.symbol_width;
+        a.C = p.chunk_size;
+        launch_shard_assemble(a, st);
+        CK(cudaGetLastError());
+        c->last_launches = 1;
+        Meta h;
+        CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h.overflow) return overflow_error(err);
+    }
+    for (uint64_t i = 0; i < ns && i < max_segs && segs; ++i)
+        for (int q = 0; q < 3; ++q) segs[3 * i + q] = sg[3 * i + q];
+    *n_segs = ns;
+    *out_len = total;
+    return PLZGPU_OK;
+}
+
+int plzgpu_shard_headers(plzgpu_ctx* c, const plzgpu_params* params, uint64_t n_total,
+                         const uint64_t* totals, const void* tail, void* d_img, uint64_t cap,
+                         uint64_t* img_len, void* stream, plzgpu_error* err) {
+    clear_err(err);
+    *img_len = 0;
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    const plzgpu_params& p = *params;
+    const Geometry g = geometry(n_total, p);
+    std::vector<HeaderDesc> hd(g.n_blocks);
+    uint64_t at = 0;
+    for (uint64_t j = 0; j < g.n_blocks; ++j) {
+        HeaderDesc& d = hd[j];
+        const uint64_t g0 = j * g.cpb;
+        d.n = uint32_t((j + 1 == g.n_blocks) ? g.n_chunks - g0 : g.cpb);
+        d.byte_len = (j + 1 == g.n_blocks) ? n_total - j * p.block_bytes : p.block_bytes;
+        d.tail_len = uint8_t(d.byte_len % uint64_t(p.symbol_width));
+        for (int i = 0; i < d.tail_len; ++i) d.tail[i] = static_cast<const uint8_t*>(tail)[i];
+        d.ptot = totals[2 * j];
+        d.ftot = totals[2 * j + 1];
+        if (d.ptot > 0xffffffffull || d.ftot > 0xffffffffull) return overflow_error(err);
+        d.img_off = at;
+        at += 26 + 8 * (uint64_t(d.n) + 1) + d.ptot + d.ftot + d.tail_len;
+    }
+    if (at > cap)
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex, "image buffer too small");
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    if (g.n_blocks) {
+        CK(c->shard_desc.ensure(g.n_blocks * sizeof(HeaderDesc)));
+        CK(cudaMemcpyAsync(c->shard_desc.p, hd.data(), g.n_blocks * sizeof(HeaderDesc),
+                           cudaMemcpyHostToDevice, st));
+        launch_shard_headers(c->shard_desc.as<HeaderDesc>(), g.n_blocks,
+                             static_cast<uint8_t*>(d_img), p.symbol_width, p.window, p.interval,
+                             p.chunk_size, st);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+    }
+    *img_len = at;
     return PLZGPU_OK;
 }
 

@@ -96,6 +96,44 @@ struct AssembleArgs {
 void launch_assemble(const AssembleArgs& a, cudaStream_t st);
 void launch_headers(const AssembleArgs& a, cudaStream_t st);
 
+// ---------------------------------------------------- multi-GPU shards
+// One container touched by a shard's chunk range [g_lo, g_hi) (local
+// chunk indices).  The shard writes four segments of the final image into a
+// local buffer: its payload-table entries, flag-table entries, flag bytes and
+// payload bytes, rebased by the bytes earlier shards contribute (p_base,
+// f_base) to the container's streams.
+struct ShardCont {
+    uint64_t g_lo, g_hi;         // local chunk range
+    uint64_t k_lo;               // container-relative index of local chunk g_lo
+    uint64_t p_base, f_base;     // shard's first byte in the container's streams
+    uint64_t seg_ptab, seg_ftab, seg_flags, seg_pay;  // local buffer offsets
+};
+struct ShardAssembleArgs {
+    const uint8_t* pay_slots;
+    const uint8_t* flag_slots;
+    const uint32_t* psize;
+    const uint32_t* fsize;
+    const uint64_t* P64;         // local exclusive prefixes (n_chunks + 1)
+    const uint64_t* F64;
+    const ShardCont* conts;
+    uint64_t n_conts;
+    uint8_t* out;
+    uint32_t* overflow;
+    uint64_t n_chunks;           // local chunk count
+    int S, C;
+};
+void launch_shard_assemble(const ShardAssembleArgs& a, cudaStream_t st);
+
+// Root side: header, final table entries and tail of every container.
+struct HeaderDesc {
+    uint64_t img_off, byte_len, ptot, ftot;
+    uint32_t n;
+    uint8_t tail_len;
+    uint8_t tail[3];
+};
+void launch_shard_headers(const HeaderDesc* d, uint64_t n_conts, uint8_t* img, int S, int W, int I,
+                          int C, cudaStream_t st);
+
 // ------------------------------------------------------------- decode side
 struct ContainerDesc {
     uint64_t img_off;            // container byte 0 in the image

@@ -1,0 +1,239 @@
+"""Multi-GPU sharded compression.
+
+Chunks are independent (no window crosses a chunk, matcher.cpp:76), so the
+partition's chunk index space is split into contiguous per-rank ranges that
+may cut through a container.  The only exchange is a handful of integers:
+
+1. every rank runs Kernels I+II on its range (``plzgpu_shard_encode``) and
+   gets, per container it touches, the payload / flag bytes it produced;
+2. one all-gather of those triples (NCCL over NVLink on GPUs) gives every rank
+   each container's stream totals, its own base offset inside each container's
+   streams, and every container's offset in the final image;
+3. every rank writes the table slices and stream slices it owns, rebased, into
+   a local buffer (``plzgpu_shard_assemble``) — four segments per container;
+4. rank 0 receives every rank's segments straight into the image at their
+   offsets (P2P sends/recvs) and writes the container headers, final table
+   entries and the tail (``plzgpu_shard_headers``).
+
+The gathered image is byte-identical to a single-GPU ``compress`` of the
+whole input (tests/test_gpu_shards.py) — and therefore to the reference.
+
+The protocol is written against two small interfaces so one driver serves
+NCCL ranks, gloo CPU tests and an in-process single-GPU simulation:
+``Backend`` (encode / assemble / segments / headers) and ``Comm``
+(all-gather of an int64 vector, point-to-point byte transfers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Sequence, Tuple
+
+from . import _lib as L
+from . import plz
+
+Totals = List[Tuple[int, int, int]]          # (container index, payload bytes, flag bytes)
+Segment = Tuple[int, int, int]               # (image offset, local offset, length)
+
+
+def chunk_ranges(n_chunks: int, world: int) -> List[Tuple[int, int]]:
+    """Balanced contiguous chunk ranges, one per rank."""
+    return [(n_chunks * r // world, n_chunks * (r + 1) // world) for r in range(world)]
+
+
+def geometry(n_total: int, params: plz.Params):
+    p = params.to_c()
+    return int(L.lib().plzgpu_num_chunks(n_total, C.byref(p))), \
+        int(L.lib().plzgpu_num_containers(n_total, C.byref(p)))
+
+
+def container_layout(n_total: int, params: plz.Params):
+    """Per container: (chunk count, byte length, tail length) — partition.cpp:5-25."""
+    return [(b.num_chunks, b.byte_len, b.tail_len) for b in plz.plan(n_total, params)]
+
+
+@dataclass
+class Plan:
+    totals: List[Tuple[int, int]]            # per container (payload total, flag total)
+    img_off: List[int]                       # per container image offset
+    image_len: int
+    bases: List[List[Tuple[int, int, int, int]]]  # per rank, per touched container:
+    # (payload_base, flag_base, container image offset, container flag total)
+
+
+def plan_offsets(n_total: int, params: plz.Params, per_rank: Sequence[Totals]) -> Plan:
+    """Global offsets from every rank's per-container totals (step 2)."""
+    layout = container_layout(n_total, params)
+    nc = len(layout)
+    ptot, ftot = [0] * nc, [0] * nc
+    bases = []
+    for tot in per_rank:
+        mine = []
+        for j, pb, fb in tot:
+            mine.append([j, ptot[j], ftot[j]])
+            ptot[j] += pb
+            ftot[j] += fb
+        bases.append(mine)
+    img_off, at = [], 0
+    for j, (n, _, tail) in enumerate(layout):
+        img_off.append(at)
+        at += 26 + 8 * (n + 1) + ptot[j] + ftot[j] + tail
+    rank_bases = [[(pb, fb, img_off[j], ftot[j]) for j, pb, fb in mine] for mine in bases]
+    return Plan(list(zip(ptot, ftot)), img_off, at, rank_bases)
+
+
+def shard_segments(params: plz.Params, n_total: int, rng: Tuple[int, int], totals: Totals,
+                   bases) -> List[Segment]:
+    """Image segments a shard owns (host arithmetic, plzgpu_shard_segments)."""
+    nt = len(totals)
+    if nt == 0:
+        return []
+    t = (C.c_uint64 * (3 * nt))(*[v for row in totals for v in row])
+    b = (C.c_uint64 * (4 * nt))(*[v for row in bases for v in row])
+    segs = (C.c_uint64 * (12 * nt))()
+    ns = L.lib().plzgpu_shard_segments(C.byref(params.to_c()), n_total, rng[0], rng[1], t, b, nt,
+                                       segs, 4 * nt)
+    return [(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2]) for i in range(ns)]
+
+
+# ------------------------------------------------------------------ backend
+class GpuBackend:
+    """The sm_100a kernels through the C-ABI; buffers are torch CUDA tensors."""
+
+    def __init__(self, params: plz.Params, device: int = 0, ctx: plz.Context = None):
+        import torch
+
+        self.torch = torch
+        self.params = params
+        self.device = torch.device("cuda", device)
+        self.ctx = ctx or plz.Context(device)
+
+    def encode(self, d_local, n_total: int, rng: Tuple[int, int], stream: int = 0) -> Totals:
+        ptr = d_local.data_ptr() if d_local is not None and d_local.numel() else 0
+        self._totals = self.ctx.shard_encode(self.params, ptr, n_total, rng[0], rng[1], stream)
+        self._rng = rng
+        return self._totals
+
+    def assemble(self, bases, stream: int = 0):
+        # local bytes = 8 table bytes per chunk + this shard's stream bytes
+        cap = 8 * (self._rng[1] - self._rng[0]) + sum(p + f for _, p, f in self._totals)
+        out = self.torch.empty(max(cap, 16), dtype=self.torch.uint8, device=self.device)
+        segs, _ = self.ctx.shard_assemble(bases, out.data_ptr(), out.numel(), stream)
+        return out, segs
+
+    def new_image(self, n: int):
+        return self.torch.empty(max(n, 16), dtype=self.torch.uint8, device=self.device)
+
+    def headers(self, n_total: int, plan: Plan, tail: bytes, img, stream: int = 0) -> int:
+        return self.ctx.shard_headers(self.params, n_total, plan.totals, tail, img.data_ptr(),
+                                      img.numel(), stream)
+
+    def copy_into(self, img, off: int, src, src_off: int, n: int):
+        img[off:off + n].copy_(src[src_off:src_off + n])
+
+
+# --------------------------------------------------------------------- comm
+class TorchComm:
+    """torch.distributed: NCCL (CUDA tensors) or gloo (CPU tensors)."""
+
+    def __init__(self, device):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.device = torch, dist, device
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+
+    def allgather(self, vec: List[int]) -> List[List[int]]:
+        t = self.torch.tensor(vec, dtype=self.torch.int64, device=self.device)
+        outs = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(outs, t)
+        return [o.tolist() for o in outs]
+
+    def gather_segments(self, img, local, my_segs, segs_by_rank):
+        """Rank 0 receives every rank's segments into img at their offsets."""
+        ops = []
+        if self.rank == 0:
+            for r in range(1, self.world):
+                for off, _, n in segs_by_rank[r]:
+                    if n:
+                        ops.append(self.dist.P2POp(self.dist.irecv, img[off:off + n], r))
+        else:
+            for _, loc, n in my_segs:
+                if n:
+                    ops.append(self.dist.P2POp(self.dist.isend, local[loc:loc + n], 0))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+def _pack(totals: Totals, tail: bytes, max_touched: int) -> List[int]:
+    vec = [-1] * (3 * max_touched) + [len(tail)] + list(tail) + [0] * (3 - len(tail))
+    for i, row in enumerate(totals):
+        vec[3 * i:3 * i + 3] = list(row)
+    return vec
+
+
+def _unpack(vec: List[int], max_touched: int):
+    totals = [tuple(vec[3 * i:3 * i + 3]) for i in range(max_touched) if vec[3 * i] >= 0]
+    tl = vec[3 * max_touched]
+    return totals, bytes(vec[3 * max_touched + 1:3 * max_touched + 1 + tl])
+
+
+def compress_sharded(backend, comm, params: plz.Params, n_total: int, d_local,
+                     tail: bytes = b"", stream: int = 0):
+    """Run the protocol on this rank; returns (image, image_len) on rank 0 and
+    (None, image_len) elsewhere.  d_local holds this rank's chunk range
+    (chunk_ranges(...)[rank]); the final rank also passes the input's last
+    n_total % S bytes as `tail`."""
+    n_chunks, _ = geometry(n_total, params)
+    ranges = chunk_ranges(n_chunks, comm.world)
+    rng = ranges[comm.rank]
+    cpb = params.block_bytes // (params.chunk_size * params.symbol_width)
+    max_touched = max((e - b + cpb - 1) // cpb + 1 for b, e in ranges)
+    mine = backend.encode(d_local, n_total, rng, stream)
+    gathered = [_unpack(v, max_touched) for v in comm.allgather(_pack(mine, tail, max_touched))]
+    per_rank = [g[0] for g in gathered]
+    tail_all = b"".join(g[1] for g in gathered)
+    plan = plan_offsets(n_total, params, per_rank)
+    local, my_segs = backend.assemble(plan.bases[comm.rank], stream)
+    img = None
+    if comm.rank == 0:
+        img = backend.new_image(plan.image_len)
+        for off, loc, n in my_segs:
+            if n:
+                backend.copy_into(img, off, local, loc, n)
+        segs_by_rank = [shard_segments(params, n_total, ranges[r], per_rank[r], plan.bases[r])
+                        for r in range(comm.world)]
+    else:
+        segs_by_rank = None
+    comm.gather_segments(img, local, my_segs, segs_by_rank)
+    if comm.rank == 0:
+        backend.headers(n_total, plan, tail_all, img, stream)
+    return img, plan.image_len
+
+
+def simulate_sharded(params: plz.Params, data, world: int, device: int = 0):
+    """Single-process run of the protocol for `world` virtual ranks on one GPU
+    (one context per rank, exchanges done in memory): the per-rank C-ABI calls,
+    offset plan and segment placement are exactly those of compress_sharded.
+    Returns the assembled image (CUDA uint8 tensor)."""
+    n_total = data.numel()
+    n_chunks, _ = geometry(n_total, params)
+    ranges = chunk_ranges(n_chunks, world)
+    S, Cs = params.symbol_width, params.chunk_size
+    backends = [GpuBackend(params, device) for _ in range(world)]
+    per_rank = []
+    for r, (b, e) in enumerate(ranges):
+        hi = n_total if e == n_chunks else e * Cs * S
+        per_rank.append(backends[r].encode(data[b * Cs * S:hi], n_total, (b, e)))
+    plan = plan_offsets(n_total, params, per_rank)
+    img = backends[0].new_image(plan.image_len)
+    for r in range(world):
+        local, segs = backends[r].assemble(plan.bases[r])
+        for off, loc, n in segs:
+            if n:
+                backends[0].copy_into(img, off, local, loc, n)
+    tail_len = n_total % S if n_total else 0
+    tail = bytes(data[n_total - tail_len:].cpu().tolist()) if tail_len else b""
+    backends[0].headers(n_total, plan, tail, img)
+    return img[:plan.image_len]

@@ -213,6 +213,38 @@ class Context:
                                                C.c_void_p(d_out), cap, C.c_void_p(d_len),
                                                C.c_void_p(stream or None), C.byref(e)), e)
 
+    # ---- multi-GPU shard protocol (paper_2304_07342_b200/dist.py)
+    def shard_encode(self, params: Params, src: int, n_total: int, begin: int, end: int,
+                     stream: int = 0):
+        maxt = 4 + (end - begin) * params.chunk_size * params.symbol_width // params.block_bytes
+        tot = (C.c_uint64 * (3 * maxt))()
+        nt, e = C.c_uint64(), L.Error()
+        _check(L.lib().plzgpu_shard_encode(self.handle, C.byref(params.to_c()), C.c_void_p(src),
+                                           n_total, begin, end, tot, maxt, C.byref(nt),
+                                           C.c_void_p(stream or None), C.byref(e)), e)
+        return [(tot[3 * i], tot[3 * i + 1], tot[3 * i + 2]) for i in range(nt.value)]
+
+    def shard_assemble(self, bases, d_out: int, cap: int, stream: int = 0):
+        nb = len(bases)
+        b = (C.c_uint64 * max(1, 4 * nb))(*[v for row in bases for v in row])
+        segs = (C.c_uint64 * max(3, 12 * nb))()
+        ns, ln, e = C.c_uint64(), C.c_uint64(), L.Error()
+        _check(L.lib().plzgpu_shard_assemble(self.handle, b, C.c_void_p(d_out), cap, segs, 4 * nb,
+                                             C.byref(ns), C.byref(ln), C.c_void_p(stream or None),
+                                             C.byref(e)), e)
+        return [(segs[3 * i], segs[3 * i + 1], segs[3 * i + 2]) for i in range(ns.value)], ln.value
+
+    def shard_headers(self, params: Params, n_total: int, totals, tail: bytes, d_img: int,
+                      cap: int, stream: int = 0) -> int:
+        nc = len(totals)
+        t = (C.c_uint64 * max(2, 2 * nc))(*[v for row in totals for v in row])
+        tb = C.create_string_buffer(bytes(tail) + b"\0" * 4, 8)
+        ln, e = C.c_uint64(), L.Error()
+        _check(L.lib().plzgpu_shard_headers(self.handle, C.byref(params.to_c()), n_total, t, tb,
+                                            C.c_void_p(d_img), cap, C.byref(ln),
+                                            C.c_void_p(stream or None), C.byref(e)), e)
+        return int(ln.value)
+
     def encode_only(self, params: Params, d_in: int, n: int, stream: int = 0) -> None:
         """Kernel I alone (profiling hook plzgpu_profile_encode)."""
         e = L.Error()

@@ -1,0 +1,131 @@
+"""CPU, world_size 2 over gloo: the multi-GPU shard protocol's host logic
+(chunk ranges, the size all-gather, offset plan, segment arithmetic of the
+C-ABI, rank-0 P2P gather and header writing) run end to end with a stand-in
+backend that cuts each rank's pieces out of the C oracle's image.  The
+assembled image must equal the oracle's (= the reference's) image."""
+import os
+import struct
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import inputs
+import oracle as O
+from paper_2304_07342_b200 import dist as D
+from paper_2304_07342_b200 import plz
+
+
+class OracleBackend:
+    """Per-rank pieces taken from a reference image (test stand-in for the
+    GPU kernels; the protocol code under test is dist.py + the C-ABI's
+    plzgpu_shard_segments)."""
+
+    def __init__(self, params, image):
+        self.params, self.img = params, image
+        self.conts = []
+        at = 0
+        while at < len(image):
+            n = struct.unpack_from("<I", image, at + 21)[0]
+            pt = struct.unpack_from(f"<{n + 1}I", image, at + 26)
+            ft = struct.unpack_from(f"<{n + 1}I", image, at + 26 + 4 * (n + 1))
+            fs = at + 26 + 8 * (n + 1)
+            self.conts.append((n, pt, ft, fs, fs + ft[n]))
+            at = fs + ft[n] + pt[n] + image[at + 25]
+        self.cpb = params.block_bytes // (params.chunk_size * params.symbol_width)
+
+    def _touched(self, rng):
+        b, e = rng
+        out = []
+        for j, (n, pt, ft, fs, ps) in enumerate(self.conts):
+            g0 = j * self.cpb
+            lo, hi = max(b, g0), min(e, g0 + n)
+            if lo < hi:
+                out.append((j, lo - g0, hi - g0))
+        return out
+
+    def encode(self, d_local, n_total, rng, stream=0):
+        self.rng = rng
+        res = []
+        for j, klo, khi in self._touched(rng):
+            n, pt, ft, _, _ = self.conts[j]
+            res.append((j, pt[khi] - pt[klo], ft[khi] - ft[klo]))
+        self.totals = res
+        return res
+
+    def assemble(self, bases, stream=0):
+        buf = bytearray()
+        for (j, klo, khi), (pb, fb, _, _) in zip(self._touched(self.rng), bases):
+            n, pt, ft, fs, ps = self.conts[j]
+            buf += b"".join(struct.pack("<I", pb + pt[k] - pt[klo]) for k in range(klo, khi))
+            buf += b"".join(struct.pack("<I", fb + ft[k] - ft[klo]) for k in range(klo, khi))
+            buf += self.img[fs + ft[klo]:fs + ft[khi]]
+            buf += self.img[ps + pt[klo]:ps + pt[khi]]
+        segs = D.shard_segments(self.params, self.n_total, self.rng, self.totals, bases)
+        assert sum(s[2] for s in segs) == len(buf)
+        return torch.frombuffer(bytearray(buf) or bytearray(1), dtype=torch.uint8), segs
+
+    def new_image(self, n):
+        return torch.zeros(max(n, 1), dtype=torch.uint8)
+
+    def copy_into(self, img, off, src, loc, n):
+        img[off:off + n].copy_(src[loc:loc + n])
+
+    def headers(self, n_total, plan, tail, img, stream=0):
+        layout = D.container_layout(n_total, self.params)
+        p = self.params
+        for j, ((n, blen, tl), (pt, ft)) in enumerate(zip(layout, plan.totals)):
+            at = plan.img_off[j]
+            hdr = b"PLZ1" + bytes([1, p.symbol_width, p.window, p.interval, 0]) + \
+                struct.pack("<IQIB", p.chunk_size, blen, n, tl)
+            img[at:at + 26] = torch.tensor(list(hdr), dtype=torch.uint8)
+            img[at + 26 + 4 * n:at + 30 + 4 * n] = torch.tensor(list(struct.pack("<I", pt)),
+                                                                dtype=torch.uint8)
+            fo = at + 26 + 4 * (n + 1) + 4 * n
+            img[fo:fo + 4] = torch.tensor(list(struct.pack("<I", ft)), dtype=torch.uint8)
+            if tl:
+                to = at + 26 + 8 * (n + 1) + pt + ft
+                img[to:to + tl] = torch.tensor(list(tail[:tl]), dtype=torch.uint8)
+        return plan.image_len
+
+
+CASES = [(2, 255, 2048, 2, 2048 * 2 * 3, 17 * 4096 + 3), (1, 128, 1024, 1, 1024 * 2, 9 * 1024 + 5),
+         (4, 64, 1024, 4, 256 << 20, 5 * 4096 + 7)]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        results = []
+        for S, W, Cs, I, bb, size in CASES:
+            p = plz.validate(plz.Params(S, W, Cs, I, bb))
+            data = inputs.make("quant", size, 7, S)
+            image = O.compress(data, O.make_params(S, W, Cs, I, bb))
+            be = OracleBackend(p, image)
+            be.n_total = len(data)
+            n_chunks, _ = D.geometry(len(data), p)
+            b, e = D.chunk_ranges(n_chunks, world)[rank]
+            tail = data[len(data) - len(data) % S:] if e == n_chunks else b""
+            img, ln = D.compress_sharded(be, D.TorchComm("cpu"), p, len(data), None, tail)
+            if rank == 0:
+                results.append(bytes(img[:ln].numpy().tobytes()) == image)
+        if rank == 0:
+            q.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_protocol_over_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + world + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert q.get(timeout=5) == [True] * len(CASES)
