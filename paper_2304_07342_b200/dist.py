@@ -150,20 +150,31 @@ class TorchComm:
         return [o.tolist() for o in outs]
 
     def gather_segments(self, img, local, my_segs, segs_by_rank):
-        """Rank 0 receives every rank's segments into img at their offsets."""
-        ops = []
+        """Rank 0 receives every rank's segments into img at their offsets
+        (zero-copy P2P on NCCL; host-staged when a CPU backend meets CUDA
+        buffers)."""
+        stage = str(self.device) == "cpu" and (
+            (img is not None and img.is_cuda) or (local is not None and local.is_cuda))
+        ops, landing = [], []
         if self.rank == 0:
             for r in range(1, self.world):
                 for off, _, n in segs_by_rank[r]:
                     if n:
-                        ops.append(self.dist.P2POp(self.dist.irecv, img[off:off + n], r))
+                        buf = self.torch.empty(n, dtype=self.torch.uint8) if stage else img[off:off + n]
+                        landing.append((off, buf))
+                        ops.append(self.dist.P2POp(self.dist.irecv, buf, r))
         else:
+            src = local.cpu() if stage else local
             for _, loc, n in my_segs:
                 if n:
-                    ops.append(self.dist.P2POp(self.dist.isend, local[loc:loc + n], 0))
+                    ops.append(self.dist.P2POp(self.dist.isend, src[loc:loc + n].clone() if stage
+                                               else src[loc:loc + n], 0))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+        if stage and self.rank == 0:
+            for off, buf in landing:
+                img[off:off + buf.numel()].copy_(buf)
 
 
 def _pack(totals: Totals, tail: bytes, max_touched: int) -> List[int]:
