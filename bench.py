@@ -370,6 +370,7 @@ def run_b200(args):
 
     total_in = n * world
     peak, peak_kind = load_peaks()
+    prof = ncu_profile_facts("plz_encode_kernel")
     enc_bytes = n + n_img  # input read + staged tokens written (~ image)
     achieved = enc_bytes / (enc_ms * 1e-3) / 1e9
     line = {
@@ -401,9 +402,14 @@ def run_b200(args):
                                "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n}},
         "roofline": {"kernel": "plz_encode_kernel (Kernel I)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_kind": peak_kind, "traffic": None,
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "traffic": prof["dram_bytes"] if prof else None,
                      "bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
-                     "note": "integer/shared-memory bound matcher; see profiles/"},
+                     "note": "Kernel I is integer-ALU bound, not HBM bound: the ALU-pipe "
+                             "utilisation below is its binding roofline (ncu, profiles/)",
+                     "alu_pipe": ({"frac": prof["alu_pipe_pct"] / 100, "issue_active":
+                                   prof["issue_active_pct"] / 100, "source": prof["source"]}
+                                  if prof and prof.get("alu_pipe_pct") else None)},
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
         "gpu_launches": (launches if world == 1 else 4) * args.steps,
         "clocks": clk.summary(),
@@ -427,6 +433,28 @@ def run_b200(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def ncu_profile_facts(kernel: str):
+    """DRAM traffic per launch and pipe utilisation of `kernel` from the newest
+    committed ncu capture (profiles/<round>/kernel_metrics.csv) — measured by
+    tools/profile_round.sh on a B200, not inside this run."""
+    import csv
+    import glob
+
+    best = None
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "kernel_metrics.csv"))):
+        with open(path) as fh:
+            for row in csv.DictReader(fh):
+                if kernel in row.get("kernel", ""):
+                    best = (path, row)
+    if not best:
+        return None
+    path, row = best
+    f = lambda k: float(row[k]) if row.get(k) not in (None, "") else None  # noqa: E731
+    return {"source": os.path.relpath(path, ROOT), "dram_bytes": (f("dram_read_B") or 0) +
+            (f("dram_write_B") or 0), "alu_pipe_pct": f("alu_pipe_pct"),
+            "issue_active_pct": f("issue_active_pct"), "sm_throughput_pct": f("sm_throughput_pct")}
 
 
 def encode_kernel_ms(ctx, params, d_in, n, img, cap, lens, stream, steps):
