@@ -26,7 +26,8 @@ namespace plzgpu {
 namespace {
 
 constexpr int kDecodeWarps = 8;
-constexpr uint32_t kDecodeSmem = 8192;  // bytes of output staging per warp
+constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 KiB chunks;
+                                        // larger chunks decode in global memory)
 constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144;  // + token table (16-B aligned)
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
@@ -70,8 +71,9 @@ struct SymOut {
 // pointers and LZ77-style replication when len > off (decoder.cpp:80-84).
 __device__ __forceinline__ int source_of(uint32_t e, uint32_t rel) {
     const uint32_t rp = e >> 16, off = e & 0xffu;
-    const uint32_t d = rel - rp;
-    return int(rp) - int(off) + int(d < off ? d : d % off);
+    uint32_t d = rel - rp;
+    if (d >= off) d %= off;  // only malformed pointers (len > off) replicate
+    return int(rp) - int(off) + int(d);
 }
 
 // Token walk of one chunk by one warp; decoded symbols go to out[0, L).
