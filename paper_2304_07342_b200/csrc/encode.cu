@@ -176,9 +176,48 @@ __device__ __forceinline__ uint32_t pair_window(const typename Sym<S>::Cell* __r
     return lo > hi ? lo : hi;
 }
 
+// Identical-cell candidates (both runs end together) continue past the run.
+// Each lane holds a bitmask of its own; the warp compacts them into a list in
+// shared memory so every lane continues at most a few, instead of a
+// divergent per-lane loop.  offset_of(bit) maps a pending bit to its offset.
+template <int S, typename OffsetOf>
+__device__ __forceinline__ uint32_t continue_pending(const typename Sym<S>::Cell* __restrict__ cells,
+                                                     int p, uint32_t cap, uint32_t rp,
+                                                     uint8_t* list, uint32_t lane,
+                                                     uint32_t pending, uint32_t best,
+                                                     OffsetOf offset_of) {
+    const uint32_t cnt = __popc(pending);
+    if (!__any_sync(0xffffffffu, cnt != 0)) return best;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= uint32_t(d)) incl += x;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t at = incl - cnt;
+    while (pending) {
+        const int b = __ffs(pending) - 1;
+        pending &= pending - 1;
+        list[at++] = uint8_t(offset_of(b));
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < total; i += 32) {
+        const int o = list[i];
+        const int ub = o < int(cap) ? o : int(cap);
+        if (int(rp) >= ub) continue;
+        const uint32_t k = uint32_t(lcp_continue<S>(cells, p - o, p, static_cast<int>(rp), ub));
+        const uint32_t key = (k << 8) | uint32_t(o);
+        best = key > best ? key : best;
+    }
+    __syncwarp();
+    return best;
+}
+
 template <int S>
 __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell* __restrict__ cells,
-                                                    int p, int n, int W, uint32_t lane) {
+                                                    int p, int n, int W, uint32_t lane,
+                                                    uint8_t* list) {
     using Cell = typename Sym<S>::Cell;
     const int lim = p < W ? p : W;  // offsets 1..lim are in the window
     const uint32_t cap = uint32_t((n - p) < 255 ? (n - p) : 255);
@@ -193,19 +232,9 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
         const uint32_t s2 = uint32_t(cell_sym<S>(cp)) * 0x00010001u, rp2 = rp * 0x00010001u;
         best = cap == 255 ? pair_window<S, false>(cells, p, lim, cap, s2, rp2, lane, pending, w0)
                           : pair_window<S, true>(cells, p, lim, cap, s2, rp2, lane, pending, w0);
-        if (__any_sync(0xffffffffu, pending != 0)) {
-            while (pending) {
-                const int b = __ffs(pending) - 1;
-                pending &= pending - 1;
-                const int w = w0 + 2 * (static_cast<int>(lane) + 32 * (b & 15)) + (b >> 4);
-                const int o = p - w;
-                const int ub = o < int(cap) ? o : int(cap);
-                if (int(rp) >= ub) continue;
-                const uint32_t k = uint32_t(lcp_continue<S>(cells, w, p, static_cast<int>(rp), ub));
-                const uint32_t key = (k << 8) | uint32_t(o);
-                best = key > best ? key : best;
-            }
-        }
+        const int wl = w0 + 2 * static_cast<int>(lane);
+        best = continue_pending<S>(cells, p, cap, rp, list, lane, pending, best,
+                                   [&](int b) { return p - (wl + 64 * (b & 15) + (b >> 4)); });
         return __reduce_max_sync(0xffffffffu, best);
     }
     if (cap == 255 && full == 7) {  // steady state of W = 255: straight-line 7 rounds + tail
@@ -222,16 +251,8 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
         eval_window<S, true>(cw, cp, rp, o0, full, cap, best, pending);
     }
     // identical cells: both runs end together, continue at relative rp
-    if (__any_sync(0xffffffffu, pending != 0)) while (pending) {
-        const int r = __ffs(pending) - 1;
-        pending &= pending - 1;
-        const int o = o0 - 32 * r;
-        const int ub = o < int(cap) ? o : int(cap);
-        if (int(rp) >= ub) continue;
-        const uint32_t k = uint32_t(lcp_continue<S>(cells, p - o, p, static_cast<int>(rp), ub));
-        const uint32_t key = (k << 8) | uint32_t(o);
-        best = key > best ? key : best;
-    }
+    best = continue_pending<S>(cells, p, cap, rp, list, lane, pending, best,
+                               [&](int b) { return o0 - 32 * b; });
     return __reduce_max_sync(0xffffffffu, best);
 }
 
@@ -256,7 +277,8 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     Cell* cells = reinterpret_cast<Cell*>(base + kHead);          // C cells (2S bytes each)
     uint8_t* raw8 = base + kHead + size_t(C) * S;                 // raw stage: upper half
     uint8_t* flg = base + kHead + size_t(C) * sizeof(Cell);       // C/8 bytes
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(flg + C / 8);    // 8B aligned
+    uint8_t* list = flg + C / 8;                                  // 256 B continuation list
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(list + 256);     // 8B aligned
 
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
@@ -272,6 +294,25 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         const int n = (g + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
         const uint32_t nbytes = uint32_t(n) * S;
         const uint8_t* src = a.in + g * uint64_t(C) * S;
+
+        // H2D pipeline: wait (bounded, ~4 s) until this chunk's segment landed
+        if (a.ready) {
+            uint32_t ok = 1;
+            if (lane == 0) {
+                const uint32_t* f = a.ready + g / a.seg_chunks;
+                const long long t0 = clock64();
+                while (ld_acquire_sys(f) != a.epoch) {
+                    __nanosleep(256);
+                    if (clock64() - t0 > (1ll << 33)) {
+                        atomicExch(a.stalled, 1u);
+                        ok = 0;
+                        break;
+                    }
+                }
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+            if (!__shfl_sync(0xffffffffu, ok, 0)) break;
+        }
 
         // ---- stage the chunk's bytes into the upper half of the cell array
         if (a.bulk_ok && (nbytes & 15u) == 0) {
@@ -315,36 +356,39 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         }
         __syncwarp();
 
-        // ---- greedy walk (encoder.cpp:25-41) with on-demand matching
+        // ---- greedy walk (encoder.cpp:25-41) with on-demand matching.  Flag
+        // bits gather in a 32-token word: token t is bit (t % 32) ^ 7 of the
+        // little-endian word, i.e. MSB-first within each byte.
         const int I = a.I, W = a.W, min_match = a.min_match;
         int p = 0;
-        uint32_t t = 0, pl = 0, fb = 0, nptr = 0;
+        uint32_t t = 0, pl = 0, fw = 0, nptr = 0;
         while (p < n) {
             uint32_t key = 0;
-            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<S>(cells, p, n, W, lane);
+            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<S>(cells, p, n, W, lane, list);
             const uint32_t k = key >> 8, o = key & 255u;
             const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
             if (lane == 0) {
-                if (ptr) {
-                    head[pl] = uint8_t(k);
-                    head[pl + 1] = uint8_t(o);
-                } else {
-                    const T v = cell_sym<S>(cells[p]);
-#pragma unroll
-                    for (int b = 0; b < S; ++b) head[pl + b] = uint8_t(v >> (8 * b));
+                const T v = cell_sym<S>(cells[p]);
+                if constexpr (S == 1) {
+                    head[pl] = ptr ? uint8_t(k) : uint8_t(v);
+                    if (ptr) head[pl + 1] = uint8_t(o);
+                } else {  // pl stays even: 16-bit stores
+                    uint16_t* h16 = reinterpret_cast<uint16_t*>(head + pl);
+                    h16[0] = ptr ? uint16_t(k | (o << 8)) : uint16_t(v);
+                    if (S == 4 && !ptr) h16[1] = uint16_t(uint32_t(v) >> 16);
                 }
             }
-            if (ptr) fb |= 0x80u >> (t & 7u);
+            fw |= (ptr ? 1u : 0u) << ((t & 31u) ^ 7u);
             pl += ptr ? 2u : uint32_t(S);
             nptr += ptr ? 1u : 0u;
             p += ptr ? static_cast<int>(k) : 1;
-            if ((t & 7u) == 7u) {
-                if (lane == 0) flg[t >> 3] = uint8_t(fb);
-                fb = 0;
+            if ((t & 31u) == 31u) {
+                if (lane == 0) reinterpret_cast<uint32_t*>(flg)[t >> 5] = fw;
+                fw = 0;
             }
             ++t;
         }
-        if ((t & 7u) != 0 && lane == 0) flg[t >> 3] = uint8_t(fb);
+        if ((t & 31u) != 0 && lane == 0) reinterpret_cast<uint32_t*>(flg)[t >> 5] = fw;
         __syncwarp();
 
         // ---- flush to the chunk's staging slots with 128-bit stores

@@ -112,6 +112,23 @@ Geometry geometry(uint64_t n, const plzgpu_params& p) {
     return g;
 }
 
+// cuStreamWriteValue32 through the runtime's driver entry point (no link-time
+// libcuda dependency: the library must also load on GPU-less hosts).
+typedef int (*StreamWriteValue32Fn)(void* stream, unsigned long long addr, uint32_t value,
+                                    unsigned int flags);
+StreamWriteValue32Fn stream_write_value32() {
+    static StreamWriteValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<StreamWriteValue32Fn>(p);
+    }();
+    return fn;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -158,6 +175,8 @@ struct Meta {
     uint64_t detail_token;
     unsigned long long err_chunk;
     uint32_t work[4];
+    uint32_t stalled;  // H2D pipeline: a segment never arrived
+    uint32_t pad;
     ParseResult parse;
 };
 
@@ -178,6 +197,12 @@ struct plzgpu_ctx {
     int enc_wpc[160] = {};   // launch shape cache per (S, C)
     int enc_ctas[160] = {};
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
+    // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
+    cudaStream_t copy_stream = nullptr;
+    DevBuf ready;
+    uint32_t epoch = 0;
+    const uint32_t* pipe_ready = nullptr;  // set while enqueueing a pipelined encode
+    uint32_t pipe_seg_chunks = 0;
     // last plzgpu_shard_encode: the range and its per-container local totals
     uint64_t sh_begin = 0, sh_end = 0, sh_n = 0;
     plzgpu_params sh_params{};
@@ -213,7 +238,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     CK(c->incl.ensure(tiles * 16 + 16));
     Meta* m = dmeta(c);
     CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
-    CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
+    CK(cudaMemsetAsync(m->work, 0, sizeof m->work + sizeof m->stalled, st));
     if (G == 0) {
         CK(cudaMemsetAsync(c->p64.p, 0, 8, st));
         CK(cudaMemsetAsync(c->f64.p, 0, 8, st));
@@ -236,6 +261,10 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.I = p.interval;
     e.min_match = std::max(1, p.min_match);
     e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
+    e.ready = c->pipe_ready;
+    e.epoch = c->epoch;
+    e.seg_chunks = c->pipe_seg_chunks;
+    e.stalled = &m->stalled;
     // warps per CTA that maximise resident warps per SM (smem-limited)
     const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
     int& wpc = c->enc_wpc[key];
@@ -618,6 +647,12 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
         b->release();
     if (c->host_meta) cudaFreeHost(c->host_meta);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    c->ready.release();
+    c->shard_desc.release();
     delete c;
 }
 
@@ -637,11 +672,7 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
     CK(cudaSetDevice(c->device));
     const cudaStream_t st = pick(c, stream);
     const uint8_t* d_in = static_cast<const uint8_t*>(in);
-    if (!is_device_ptr(in)) {
-        CK(c->in.ensure(n));
-        CK(cudaMemcpyAsync(c->in.p, in, n, cudaMemcpyHostToDevice, st));
-        d_in = c->in.as<uint8_t>();
-    }
+    const bool host_in = !is_device_ptr(in);
     const uint64_t bound = plzgpu_compress_bound(n, params);
     const bool direct = is_device_ptr(out) && cap >= bound;
     uint8_t* img = static_cast<uint8_t*>(out);
@@ -650,11 +681,57 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
         img = c->img.as<uint8_t>();
     }
     Meta* m = dmeta(c);
-    rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
-    if (rc) return rc;
+    const Geometry geo = geometry(n, *params);
+    const uint64_t seg_bytes_target = uint64_t(32) << 20;
+    const uint64_t chunk_bytes = uint64_t(params->chunk_size) * params->symbol_width;
+    const uint64_t seg_chunks = std::max<uint64_t>(1, seg_bytes_target / chunk_bytes);
+    const uint64_t nseg = (geo.n_chunks + seg_chunks - 1) / seg_chunks;
+    StreamWriteValue32Fn write_value = stream_write_value32();
+    if (host_in && write_value && nseg > 1) {
+        // H2D pipeline: Kernel I starts at once and each warp waits for its
+        // chunk's segment; segments land on the copy stream, each followed by
+        // a stream memory write of its ready flag.
+        CK(c->in.ensure(n));
+        CK(c->ready.ensure(nseg * 4));
+        if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        d_in = c->in.as<uint8_t>();
+        ++c->epoch;
+        if (c->epoch == 0) {  // never reuse the initial 0 flags
+            CK(cudaMemsetAsync(c->ready.p, 0, nseg * 4, st));
+            CK(cudaStreamSynchronize(st));
+            ++c->epoch;
+        }
+        c->pipe_ready = c->ready.as<uint32_t>();
+        c->pipe_seg_chunks = uint32_t(seg_chunks);
+        rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
+        c->pipe_ready = nullptr;
+        if (rc) return rc;
+        for (uint64_t sgi = 0; sgi < nseg; ++sgi) {
+            const uint64_t lo = sgi * seg_chunks * chunk_bytes;
+            const uint64_t hi = sgi + 1 == nseg ? n : std::min(n, (sgi + 1) * seg_chunks * chunk_bytes);
+            CK(cudaMemcpyAsync(c->in.as<uint8_t>() + lo, static_cast<const uint8_t*>(in) + lo,
+                               hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
+            if (write_value(c->copy_stream,
+                            reinterpret_cast<unsigned long long>(c->ready.as<uint32_t>() + sgi),
+                            c->epoch, 0) != 0)
+                return set_err(err, PLZGPU_CUDA, 0, kNoIndex, kNoIndex,
+                               "cuStreamWriteValue32 failed");
+        }
+    } else {
+        if (host_in) {
+            CK(c->in.ensure(n));
+            CK(cudaMemcpyAsync(c->in.p, in, n, cudaMemcpyHostToDevice, st));
+            d_in = c->in.as<uint8_t>();
+        }
+        rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
+        if (rc) return rc;
+    }
     Meta* h = c->host_meta;
     CK(cudaMemcpyAsync(h, m, sizeof(Meta), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (h->stalled)
+        return set_err(err, PLZGPU_CUDA, 0, kNoIndex, kNoIndex,
+                       "H2D pipeline stalled: an input segment never arrived");
     if (h->overflow) return overflow_error(err);
     if (h->img_len > cap)
         return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,

@@ -34,12 +34,13 @@ constexpr int kScanTile = kScanThreads * kScanItems;  // chunks per look-back ti
 // Per-warp shared-memory bytes of the encode kernel for chunk size C, width S:
 // C (symbol, run) cells of 2S bytes (the raw chunk is staged in their upper
 // half), a kEncodeHeadPerS*S-byte payload head (the rest of the payload
-// spills into dead cells), C/8 flag bytes and an mbarrier.
+// spills into dead cells), C/8 flag bytes, a 256-byte continuation list and
+// an mbarrier.
 constexpr uint32_t kEncodeHeadPerS = 512;  // >= 2*W + 1 for W <= 255
 __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
     // + 64 cells of slack: the last partial round of pair candidates may read
     // (and discard) up to 62 cells past the chunk end
-    size_t b = size_t(C) * 2 * S + size_t(kEncodeHeadPerS) * S + size_t(C) / 8 + 16 + 128 * S;
+    size_t b = size_t(C) * 2 * S + size_t(kEncodeHeadPerS) * S + size_t(C) / 8 + 256 + 16 + 128 * S;
     return (b + 15) & ~size_t(15);
 }
 
@@ -56,6 +57,12 @@ struct EncodeArgs {
     int C, W, I, min_match;
     int bulk_ok;                 // input base 16B-aligned: TMA bulk loads allowed
     int warps_per_cta;
+    // optional H2D pipeline: chunk g may be read once ready[g / seg_chunks]
+    // == epoch (written by a stream memory operation after its segment's copy)
+    const uint32_t* ready;
+    uint32_t epoch;
+    uint32_t seg_chunks;
+    uint32_t* stalled;           // set if a segment never arrives (bounded wait)
 };
 void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
 int encode_ctas_per_sm(int S, int C, int warps_per_cta);
