@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libplzgpu.so")
+LIB_PATH = os.environ.get("PLZGPU_LIB") or os.path.join(HERE, "lib", "libplzgpu.so")
 
 OK, VALIDATION, UNSUPPORTED_FORMAT, CORRUPTION, CONTRACT, CUDA, CAPACITY = range(7)
 NO_INDEX = (1 << 64) - 1

@@ -28,23 +28,7 @@ namespace {
 constexpr int kDecodeWarps = 8;
 constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 KiB chunks;
                                         // larger chunks decode in global memory)
-constexpr uint32_t kStageSlack = 32;    // payload staged to end at kDecodeSmem + slack
-constexpr uint32_t kFlagStage = 288;    // flag slice staging (C/8 <= 256 + alignment)
-constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kStageSlack + kFlagStage + 144;  // + tab
-
-// Copy [src, src+n) into shared memory as its enclosing 16-byte-aligned
-// superset ending at dst_end (16-aligned); returns where src's first byte
-// landed.  128-bit loads and stores.
-__device__ __forceinline__ const uint8_t* stage_slice(uint8_t* dst_end, const uint8_t* src,
-                                                      uint64_t n, uint32_t lane) {
-    const uintptr_t a0 = reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15);
-    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src) + n + 15) & ~uintptr_t(15);
-    const uint32_t words = uint32_t((a1 - a0) >> 4);
-    uint4* d = reinterpret_cast<uint4*>(dst_end) - words;
-    const uint4* s = reinterpret_cast<const uint4*>(a0);
-    for (uint32_t i = lane; i < words; i += 32) d[i] = __ldg(s + i);
-    return reinterpret_cast<const uint8_t*>(d) + (reinterpret_cast<uintptr_t>(src) - a0);
-}
+constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144;  // + token table (16-B aligned)
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -103,8 +87,8 @@ __device__ __forceinline__ int source_of(uint32_t e, uint32_t rel) {
 // wave (earlier waves and literals are already final).  `tab` is the warp's
 // 33-entry token table in shared memory: relpos << 16 | is_ptr << 8 | off.
 template <int S, bool kBytes>
-__device__ uint32_t decode_chunk_warp(const uint8_t* flags, uint64_t nf,
-                                      const uint8_t* pay, uint64_t np, uint64_t L,
+__device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_t nf,
+                                      const uint8_t* __restrict__ pay, uint64_t np, uint64_t L,
                                       SymOut<S, kBytes> out, uint32_t* tab, uint32_t lane,
                                       uint64_t* err_tok) {
     using T = typename Sym<S>::T;
@@ -434,20 +418,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     const uint8_t* py = a.img + d.payload_off + p0;
     uint64_t tok = 0;
     uint32_t e;
-    uint8_t* fstage = stage + kDecodeSmem + kStageSlack;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(fstage + kFlagStage);
-    if (in_smem) {
-        // slices into shared memory: the payload ends at the top of the output
-        // staging, so decoding runs in place.  For S >= 2 every token advances
-        // S*pos at least as far as the payload it consumes (literal S/S,
-        // pointer S*len >= 2), so S*pos - consumed only grows to C*S - np and
-        // the write position never passes unread payload.  (S = 1 admits
-        // 1-symbol pointers in malformed streams: read from global.)
-        if (S >= 2 && p1 - p0 <= kDecodeSmem)
-            py = stage_slice(stage + kDecodeSmem + kStageSlack, py, p1 - p0, lane);
-        if (f1 - f0 + 30 <= kFlagStage) fl = stage_slice(fstage + kFlagStage, fl, f1 - f0, lane);
-        __syncwarp();
-    }
+    uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem);
     if (in_smem)
         e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{stage}, tab,
                                         lane, &tok);
