@@ -209,6 +209,24 @@ int plzgpu_shard_headers(plzgpu_ctx* ctx, const plzgpu_params* params, uint64_t 
                          const uint64_t* totals, const void* tail, void* d_img, uint64_t cap,
                          uint64_t* img_len, void* stream, plzgpu_error* err);
 
+/* ------------------------------------------------ statistics / matcher */
+
+/* replaces plz::match_chunk (matcher.hpp:49-50, matcher.cpp:113-131) over a
+ * whole input: len_out/off_out (host or device, n/S entries) receive the
+ * record of every symbol of every chunk (chunk g's symbol i at g*C + i):
+ * interval-aligned positions hold the longest match (ties to the largest
+ * offset, {0,0} for none), others the forced literal {1,0}.  raw_hist (host,
+ * 256 u64, may be NULL) tallies the lengths of records with offset != 0
+ * (match_length_histogram raw mode, corpus.cpp:199-204). */
+int plzgpu_match_table(plzgpu_ctx* ctx, const plzgpu_params* params, const void* in, uint64_t n,
+                       void* len_out, void* off_out, uint64_t* raw_hist, void* stream,
+                       plzgpu_error* err);
+
+/* Lengths of the pointer tokens compress would emit (corpus.cpp:205-217,
+ * match_length_histogram encoded mode): hist[len] counts, 256 u64 (host). */
+int plzgpu_pointer_histogram(plzgpu_ctx* ctx, const plzgpu_params* params, const void* in,
+                             uint64_t n, uint64_t* hist, void* stream, plzgpu_error* err);
+
 /* ------------------------------------------------------ profiling hook */
 
 /* Enqueue Kernel I (match + encode) alone on a device input, so its share of

@@ -53,7 +53,7 @@ class BlockPlan(C.Structure):
 
 # (name, restype, argtypes) of every exported symbol of include/plzgpu.h
 _P, _E, _U64, _VP = C.POINTER(Params), C.POINTER(Error), C.c_uint64, C.c_void_p
-SIGNATURES = [
+SIGNATURES = [  # every entry point of include/plzgpu.h
     ("plzgpu_abi_version", C.c_int, []),
     ("plzgpu_validate", C.c_int, [_P, _P, _E]),
     ("plzgpu_level_to_window", C.c_int, [C.c_int, C.POINTER(C.c_int32), _E]),
@@ -74,6 +74,8 @@ SIGNATURES = [
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),
     ("plzgpu_decompress_chunk", C.c_int, [_VP, _VP, _U64, _VP, _U64, _U64, _P, _U64, _VP, _E]),
     ("plzgpu_profile_encode", C.c_int, [_VP, _P, _VP, _U64, _VP, _E]),
+    ("plzgpu_match_table", C.c_int, [_VP, _P, _VP, _U64, _VP, _VP, C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_pointer_histogram", C.c_int, [_VP, _P, _VP, _U64, C.POINTER(_U64), _VP, _E]),
     ("plzgpu_num_chunks", _U64, [_U64, _P]),
     ("plzgpu_num_containers", _U64, [_U64, _P]),
     ("plzgpu_shard_encode", C.c_int, [_VP, _P, _VP, _U64, _U64, _U64, C.POINTER(_U64), _U64,

@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
                     if (S == 4 && !ptr) h16[1] = uint16_t(uint32_t(v) >> 16);
                 }
             }
+            if (a.hist && ptr && lane == 0) atomicAdd(&a.hist[k], 1ull);
             fw |= (ptr ? 1u : 0u) << ((t & 31u) ^ 7u);
             pl += ptr ? 2u : uint32_t(S);
             nptr += ptr ? 1u : 0u;
@@ -413,7 +414,99 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     }
 }
 
+// Full per-position match table of every chunk (matcher.cpp:113-131: aligned
+// positions searched, others the forced literal {1, 0}) — the statistics /
+// verification path (match_length_histogram raw mode), not the codec.  Same
+// staging and find_match_warp as Kernel I; one warp per chunk.
+template <int S>
+__global__ void __launch_bounds__(512) plz_match_table_kernel(EncodeArgs a, uint8_t* len_out,
+                                                              uint8_t* off_out,
+                                                              unsigned long long* raw_hist) {
+    using T = typename Sym<S>::T;
+    using Cell = typename Sym<S>::Cell;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = lane_id();
+    const int C = a.C;
+    constexpr uint32_t kHead = kEncodeHeadPerS * S;
+    uint8_t* base = smem + encode_warp_smem(C, S) * (threadIdx.x >> 5);
+    Cell* cells = reinterpret_cast<Cell*>(base + kHead);
+    uint8_t* raw8 = base + kHead + size_t(C) * S;
+    uint8_t* list = base + kHead + size_t(C) * sizeof(Cell) + C / 8;
+    for (;;) {
+        uint64_t g = 0;
+        if (lane == 0) g = atomicAdd(a.work, 1u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        if (g >= a.n_chunks) break;
+        const int n = (g + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
+        const uint8_t* src = a.in + g * uint64_t(C) * S;
+        for (uint32_t i = lane; i < uint32_t(n) * S; i += 32) raw8[i] = src[i];
+        __syncwarp();
+        const T* raw = reinterpret_cast<const T*>(raw8);
+        for (int w = 0; w <= (n - 1) >> 5; ++w) {
+            const int i = (w << 5) + static_cast<int>(lane);
+            const T v = i < n ? raw[i] : T(0);
+            __syncwarp();
+            if (i < n) cells[i] = Cell(v);
+            __syncwarp();
+        }
+        uint32_t carry = 0;
+        for (int w = (n - 1) >> 5; w >= 0; --w) {
+            const int i = (w << 5) + static_cast<int>(lane);
+            const T v = i < n ? cell_sym<S>(cells[i]) : T(0);
+            const bool eq = (i + 1 < n) && cell_sym<S>(cells[i + 1]) == v;
+            const uint32_t m = __ballot_sync(0xffffffffu, eq);
+            const uint32_t sh = m >> lane;
+            uint32_t r = sh == (0xffffffffu >> lane) ? (32u - lane) + carry
+                                                     : static_cast<uint32_t>(__ffs(~sh));
+            r = r < 255u ? r : 255u;
+            carry = __shfl_sync(0xffffffffu, r, 0);
+            __syncwarp();
+            if (i < n) cells[i] = make_cell<S>(v, r);
+        }
+        __syncwarp();
+        const uint64_t out0 = g * uint64_t(C);
+        for (int p = 0; p < n; ++p) {
+            uint32_t k = 1, o = 0;  // forced literal (matcher.cpp:121-123)
+            if ((p & (a.I - 1)) == 0) {
+                const uint32_t key = p > 0 ? find_match_warp<S>(cells, p, n, a.W, lane, list) : 0u;
+                k = key >> 8;
+                o = key & 255u;
+                if (k == 0) o = 0;  // {0, 0}: no match (matcher.cpp:109)
+            }
+            if (lane == 0) {
+                len_out[out0 + p] = uint8_t(k);
+                off_out[out0 + p] = uint8_t(o);
+                if (raw_hist && o != 0 && k > 0) atomicAdd(&raw_hist[k], 1ull);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace
+
+void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
+                        unsigned long long* raw_hist, cudaStream_t st) {
+    const size_t smem = encode_warp_smem(a.C, S) * a.warps_per_cta;
+    const dim3 block(a.warps_per_cta * 32);
+    switch (S) {
+        case 1:
+            cudaFuncSetAttribute(plz_match_table_kernel<1>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            plz_match_table_kernel<1><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
+            break;
+        case 2:
+            cudaFuncSetAttribute(plz_match_table_kernel<2>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            plz_match_table_kernel<2><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
+            break;
+        default:
+            cudaFuncSetAttribute(plz_match_table_kernel<4>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            plz_match_table_kernel<4><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
+            break;
+    }
+}
 
 int encode_ctas_per_sm(int S, int C, int warps_per_cta) {
     int blocks = 0;

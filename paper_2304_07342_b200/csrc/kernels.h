@@ -63,8 +63,12 @@ struct EncodeArgs {
     uint32_t epoch;
     uint32_t seg_chunks;
     uint32_t* stalled;           // set if a segment never arrives (bounded wait)
+    unsigned long long* hist;    // optional: selected pointer lengths [256]
 };
 void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+// full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
+void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
+                        unsigned long long* raw_hist, cudaStream_t st);
 int encode_ctas_per_sm(int S, int C, int warps_per_cta);
 
 struct ScanArgs {

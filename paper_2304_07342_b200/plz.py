@@ -384,3 +384,79 @@ def decompress_chunk(flags, payload, logical_len: int, params: Params, chunk_ind
 def compression_ratio(n_in: int, n_out: int) -> float:
     """ratio = input bytes / whole-image bytes (tools/plz.cpp:79-81)."""
     return n_in / n_out if n_out else 0.0
+
+
+# ------------------------------------------------- matcher / statistics / tuner
+def match_table(data, params: Params):
+    """plz::match_chunk over every chunk of `data` on the GPU: (length, offset)
+    per symbol (matcher.cpp:113-131) as two bytes objects."""
+    ptr, n, keep = _as_host(data)
+    nsym = n // params.symbol_width
+    ln = C.create_string_buffer(max(1, nsym))
+    of = C.create_string_buffer(max(1, nsym))
+    e = L.Error()
+    _check(L.lib().plzgpu_match_table(context().handle, C.byref(params.to_c()), C.c_void_p(ptr), n,
+                                      ln, of, None, None, C.byref(e)), e)
+    return ln.raw[:nsym], of.raw[:nsym]
+
+
+@dataclass
+class MatchHistogram:
+    """plz::MatchHistogram (corpus.hpp:33-39)."""
+
+    counts: List[int]
+    total_pointers: int
+    symbol_width: int
+    fraction_gt_128: float
+    fraction_gt_256: float
+
+
+def match_length_histogram(data, params: Params, raw_table: bool = False) -> MatchHistogram:
+    """plz::match_length_histogram (corpus.cpp:75-129), interval forced to 1."""
+    p = validate(Params(params.symbol_width, params.window, params.chunk_size, 1,
+                        params.block_bytes))
+    ptr, n, keep = _as_host(data)
+    hist = (C.c_uint64 * 256)()
+    e = L.Error()
+    if raw_table:
+        _check(L.lib().plzgpu_match_table(context().handle, C.byref(p.to_c()), C.c_void_p(ptr), n,
+                                          None, None, hist, None, C.byref(e)), e)
+    else:
+        _check(L.lib().plzgpu_pointer_histogram(context().handle, C.byref(p.to_c()),
+                                                C.c_void_p(ptr), n, hist, None, C.byref(e)), e)
+    counts = [0] + [int(hist[i]) for i in range(1, 256)]
+    total = sum(counts)
+    s = p.symbol_width
+    f128 = sum(c for l, c in enumerate(counts) if l * s > 128) / total if total else 0.0
+    f256 = sum(c for l, c in enumerate(counts) if l * s > 256) / total if total else 0.0
+    return MatchHistogram(counts, total, s, f128, f256)
+
+
+@dataclass
+class PilotReport:
+    field_ratios: List[float]
+    average: float
+    chosen: Params
+
+
+def select_params(fields, declared_width: int, base: Params, threshold: float = 1.5,
+                  pilot_cap: int = 4 << 20) -> PilotReport:
+    """plz::select_params (tuner.cpp:10-45): GPU pilot compressions."""
+    if not fields:
+        raise ValidationError("tuner requires at least one field")
+    if declared_width not in (1, 2, 4):
+        raise ValidationError("declared_width must be 1, 2 or 4")
+    pilot = validate(Params(declared_width, base.window, base.chunk_size, base.interval,
+                            base.block_bytes))
+    ratios = []
+    for f in fields:
+        sample = bytes(f[:pilot_cap])
+        img = compress(sample, pilot)
+        ratios.append(len(sample) / len(img) if img else 1.0)
+    avg = sum(ratios) / len(ratios)
+    if avg < threshold:
+        chosen = Params(1, base.window, base.chunk_size, base.interval, base.block_bytes)
+    else:
+        chosen = Params(declared_width, min(255, base.window * declared_width), base.chunk_size,
+                        base.interval, base.block_bytes)
+    return PilotReport(ratios, avg, validate(chosen))

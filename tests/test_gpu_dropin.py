@@ -1,9 +1,10 @@
-"""GPU: the reference's OWN public-API unit tests (test_params.cpp,
-test_partition.cpp, test_format.cpp, test_decoder.cpp from
-/root/reference/proj/tests, unmodified) compiled against the B200 drop-in
-headers include/plz/*.hpp and linked with libplzgpu.so (oracle/Makefile
-target dropin-tests; the binary is built in the development container and
-travels to the GPU box)."""
+"""GPU: the reference's OWN unit tests of the API the drop-in provides —
+test_params, test_partition, test_format, test_decoder, test_matcher (incl.
+3,000 random positions vs a brute-force matcher, now on the GPU matcher),
+test_corpus and test_tuner from /root/reference/proj/tests, unmodified —
+compiled against include/plz/*.hpp and linked with libplzgpu.so
+(oracle/Makefile target dropin-tests; built in the development container,
+travels to the GPU box).  49 cases / ~840k checks."""
 import os
 import subprocess
 

@@ -16,7 +16,12 @@ t0 = time.time()
 d_in = datagen.quant_codes(w, 42, "cuda")
 torch.cuda.synchronize()
 print(f"{w.name}: {d_in.numel()/1e6:.1f} MB generated in {time.time()-t0:.1f}s", flush=True)
-p = plz.validate(plz.Params(w.S, w.W, w.C, w.I))
+import os
+W = int(os.environ.get("PROBE_W", w.W))
+I = int(os.environ.get("PROBE_I", w.I))
+p = plz.validate(plz.Params(w.S, W, w.C, I))
+if W != w.W or I != w.I:
+    print(f"override W={W} I={I}")
 ctx = plz.context()
 cap = plz.compress_bound(d_in.numel(), p)
 img = torch.empty(cap, dtype=torch.uint8, device="cuda")
