@@ -174,7 +174,8 @@ struct Meta {
     uint64_t detail_chunk;
     uint64_t detail_token;
     unsigned long long err_chunk;
-    uint32_t work[4];
+    uint32_t work[8];  // [0] encode, [1] scan tiles, [2] assemble/decode, [4] fallback
+                       // count, [5] wide-pass counter
     uint32_t stalled;  // H2D pipeline: a segment never arrived
     uint32_t pad;
     ParseResult parse;
@@ -194,8 +195,9 @@ struct plzgpu_ctx {
     int last_launches = 0;
     LastOp last_op = OP_NONE;
     DecodeArgs last_decode{};
-    int enc_wpc[160] = {};   // launch shape cache per (S, C)
-    int enc_ctas[160] = {};
+    int enc_wpc[320] = {};   // launch shape cache per (S, C, dictionary)
+    int enc_ctas[320] = {};
+    DevBuf fb;               // chunks the dictionary pass left to the wide pass
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
     cudaStream_t copy_stream = nullptr;
@@ -218,6 +220,29 @@ namespace {
 cudaStream_t pick(plzgpu_ctx*, void* s) { return static_cast<cudaStream_t>(s); }
 
 Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
+
+// Launch shape of Kernel I for (S, C, dictionary), cached per context: warps
+// per CTA that maximise resident warps per SM (shared-memory limited).
+void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, bool dict, int* wpc_out,
+                  int* per_sm_out) {
+    const int key = (dict ? 160 : 0) + p.symbol_width * 32 +
+                    (__builtin_ctz(unsigned(p.chunk_size)) - 10);
+    int& wpc = c->enc_wpc[key];
+    int& per_sm = c->enc_ctas[key];
+    if (wpc == 0) {
+        int best_warps = 0;
+        for (int cand = 1; cand <= 16; ++cand) {
+            const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand, dict);
+            if (ctas * cand > best_warps) {
+                best_warps = ctas * cand;
+                wpc = cand;
+                per_sm = ctas;
+            }
+        }
+    }
+    *wpc_out = wpc;
+    *per_sm_out = per_sm;
+}
 
 // Enqueue Kernels I-III for a device-resident input.  img must hold
 // compress_bound bytes; img_len receives the image length on the device.
@@ -268,27 +293,32 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
     e.hist = c->enc_hist;
-    // warps per CTA that maximise resident warps per SM (smem-limited)
-    const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
-    int& wpc = c->enc_wpc[key];
-    int& per_sm = c->enc_ctas[key];
-    if (wpc == 0) {
-        int best_warps = 0;
-        for (int cand = 1; cand <= 16; ++cand) {
-            const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
-            if (ctas * cand > best_warps) {
-                best_warps = ctas * cand;
-                wpc = cand;
-                per_sm = ctas;
-            }
-        }
+    // S in {2, 4}: dictionary pass, then the wide pass over the chunks it left
+    const bool dict = p.symbol_width > 1;
+    if (dict) {
+        CK(c->fb.ensure(G * 4 + 16));
+        e.fb_list = c->fb.as<uint32_t>();
+        e.fb_count = &m->work[4];
     }
+    int wpc = 1, per_sm = 1;
+    encode_shape(c, p, dict, &wpc, &per_sm);
     e.warps_per_cta = wpc;
-    uint64_t grid = uint64_t(c->sms) * uint64_t(per_sm);
-    const uint64_t need = (G + wpc - 1) / wpc;
-    if (grid > need) grid = need;
-    launch_encode(p.symbol_width, e, int(grid), st);
+    launch_encode(p.symbol_width, e, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
+                                                          (G + wpc - 1) / wpc)),
+                  st, dict);
     ++*launches;
+    if (dict) {
+        EncodeArgs f = e;
+        f.from_list = 1;
+        f.work = &m->work[5];
+        f.ready = nullptr;  // every segment has landed once the dictionary pass ends
+        encode_shape(c, p, false, &wpc, &per_sm);
+        f.warps_per_cta = wpc;
+        launch_encode(p.symbol_width, f, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
+                                                              (G + wpc - 1) / wpc)),
+                      st, false);
+        ++*launches;
+    }
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
     ScanArgs sa{};
@@ -1159,26 +1189,6 @@ int plzgpu_shard_headers(plzgpu_ctx* c, const plzgpu_params* params, uint64_t n_
 
 // --------------------------------------------------- statistics / matcher
 
-// Launch shape of Kernel I for (S, C), cached per context.
-static void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int* wpc_out, int* per_sm_out) {
-    const int key = p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
-    int& wpc = c->enc_wpc[key];
-    int& per_sm = c->enc_ctas[key];
-    if (wpc == 0) {
-        int best_warps = 0;
-        for (int cand = 1; cand <= 16; ++cand) {
-            const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
-            if (ctas * cand > best_warps) {
-                best_warps = ctas * cand;
-                wpc = cand;
-                per_sm = ctas;
-            }
-        }
-    }
-    *wpc_out = wpc;
-    *per_sm_out = per_sm;
-}
-
 int plzgpu_match_table(plzgpu_ctx* c, const plzgpu_params* params, const void* in, uint64_t n,
                        void* len_out, void* off_out, uint64_t* raw_hist, void* stream,
                        plzgpu_error* err) {
@@ -1217,7 +1227,7 @@ int plzgpu_match_table(plzgpu_ctx* c, const plzgpu_params* params, const void* i
     e.I = p.interval;
     e.min_match = std::max(1, p.min_match);
     int wpc = 1, per_sm = 1;
-    encode_shape(c, p, &wpc, &per_sm);
+    encode_shape(c, p, false, &wpc, &per_sm);
     e.warps_per_cta = wpc;
     uint64_t grid = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (g.n_chunks + wpc - 1) / wpc);
     launch_match_table(p.symbol_width, e, int(grid), dl, dof,

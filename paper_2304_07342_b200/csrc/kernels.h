@@ -44,6 +44,22 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
     return (b + 15) & ~size_t(15);
 }
 
+// Dictionary layout of Kernel I for S in {2, 4} (plz_encode_kernel<S, true>):
+// the chunk's symbols are renamed to 8-bit ids (slot of a 256-entry hash
+// table), so cells are 16-bit (id, run) and matching runs the S = 1 code.
+//   [payload head: H][cells: C x 2 B][flags: C/8][list: 256][mbar: 16]
+//   [keys: 256 x u32][occupancy: 8 x u32]
+// H >= S*(p+1) - 2*(p-W) for every step p: 2W+2 for S = 2, 2C+2W+4 for S = 4
+// (S = 4 also lands its 4C raw bytes over head + cells and converts them
+// right to left).
+__host__ __device__ inline size_t encode_dict_head(int C, int S) {
+    return S == 2 ? 512 : size_t(2) * C + 512;
+}
+__host__ __device__ inline size_t encode_dict_warp_smem(int C, int S) {
+    size_t b = encode_dict_head(C, S) + size_t(C) * 2 + size_t(C) / 8 + 256 + 16 + 1024 + 32;
+    return (b + 15) & ~size_t(15);
+}
+
 struct EncodeArgs {
     const uint8_t* in;           // byte 0 of global chunk 0
     uint8_t* pay_slots;          // chunk g payload staged at g * C * S
@@ -64,12 +80,18 @@ struct EncodeArgs {
     uint32_t seg_chunks;
     uint32_t* stalled;           // set if a segment never arrives (bounded wait)
     unsigned long long* hist;    // optional: selected pointer lengths [256]
+    // dictionary pass: chunks with > 256 distinct symbols are appended to
+    // fb_list; the wide pass then takes its chunks from fb_list[0..*fb_count)
+    uint32_t* fb_list;
+    uint32_t* fb_count;
+    int from_list;               // wide pass: iterate fb_list instead of 0..n_chunks
 };
-void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+// dict: the 8-bit dictionary kernel (S in {2, 4}); otherwise the wide-cell kernel
+void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st, bool dict = false);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
 void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
                         unsigned long long* raw_hist, cudaStream_t st);
-int encode_ctas_per_sm(int S, int C, int warps_per_cta);
+int encode_ctas_per_sm(int S, int C, int warps_per_cta, bool dict = false);
 
 struct ScanArgs {
     const uint32_t* psize;

@@ -101,6 +101,39 @@ def test_configs_bit_exact(S, W, C, I, kind):
     assert plz.decompress_bytes(got) == data
 
 
+@pytest.mark.parametrize("S,C", [(2, 2048), (2, 1024), (4, 1024), (4, 4096)])
+def test_symbol_dictionary_boundary(S, C):
+    # Kernel I renames a chunk's symbols to 8-bit ids; chunks with more than
+    # 256 distinct symbols go to the wide-cell pass.  Chunks with 1, 7, 255,
+    # 256, 257 and C distinct symbols (extremes of the value range included),
+    # interleaved, must all give the reference image.
+    import numpy as np
+
+    rng = np.random.default_rng(S * 100000 + C)
+    top = (1 << (8 * S)) - 1
+    chunks = []
+    for d in (7, 256, 257, 1, 255, C, 256, 3):
+        if d == 1:
+            alphabet = np.array([top], dtype=np.uint64)
+        else:
+            pool = np.unique(rng.integers(1, top, 4 * d, dtype=np.uint64))
+            alphabet = np.concatenate([rng.permutation(pool)[: d - 2],
+                                       np.array([0, top], dtype=np.uint64)])
+        idx = np.concatenate([np.arange(d), rng.integers(0, d, C - d)])  # every symbol once
+        idx = np.repeat(idx, rng.integers(1, 4, C))[:C]  # some runs
+        idx[:d] = np.arange(d)
+        chunks.append(alphabet[idx].astype(f"<u{S}"))
+    data = np.concatenate(chunks).tobytes()
+    for W, I in ((255, 1), (64, 2)):
+        p = P(S, W, C, I)
+        want, st_ref = ref_compress(data, p)
+        stats = plz.PipelineStats()
+        got = plz.compress(data, p, stats=stats)
+        assert got == want, f"S={S} C={C} W={W} I={I}"
+        assert (stats.pointer_tokens, stats.literal_tokens) == st_ref[1:]
+        assert plz.decompress_bytes(got) == data
+
+
 def test_multi_block_images():
     # test_decoder.cpp:198-207: two chunks per block, five blocks and a tail
     p = P(2, 64, 1024, 1, 1024 * 2 * 2)
