@@ -1,0 +1,347 @@
+// bitmatch.cu — Kernel I, bitmap pass: match + greedy token walk + encode,
+// one warp per chunk, bit-parallel (shift-and) longest-match search.
+//
+// Reference contract, identical to encode.cu:
+//   matcher.cpp:71-111   longest match over w in [max(0,p-W), p), length
+//                        k(w) = min(lcp(w,p), p-w, 255, n-p), ties to the
+//                        largest offset (smallest w, strict '>' scanning up);
+//   matcher.cpp:113-131  positions with p % I != 0 are forced literals;
+//   encoder.cpp:18-73    greedy walk from 0: pointer iff off != 0 and
+//                        len >= min_match, MSB-first flag bits, pointer wire
+//                        order [len][off], literal = the S raw bytes.
+//
+// Search as set intersection.  For the position p being searched, number the
+// window candidates by bit b = w - (p - W), b in [0, W).  With
+//   A_0     = { b : w >= 0 }
+//   A_{j+1} = A_j  ∩  { b : x[w + j] == x[p + j] }  ∩  { b : p - w >= j + 1 }
+// candidate w has k(w) >= j iff b ∈ A_j, so the match length is the last j
+// with A_j non-empty and the reference's tie-break (largest offset) is the
+// LOWEST set bit of that A_K.  The middle set is a 256-bit window of the
+// occurrence bitmap of symbol x[p+j] — one funnel shift of two shared words
+// per 32 candidates — so a step costs O(W/32) word operations whatever the
+// data, and the steps of one search sum to the match length: a chunk costs
+// O(C * W / 32) word operations in total.
+//
+// Warp mapping: NW = ceil(W/32) (rounded to 1/2/4/8) lanes hold the NW words
+// of a candidate set; the warp's G = 32/NW lane groups evaluate G consecutive
+// steps j..j+G-1 at once and an AND prefix over the groups (shfl_up) gives
+// A_{j+1..j+G}; one ballot tells how many of them are non-empty.
+//
+// Occurrence bitmaps need one row per distinct symbol of the chunk (quant
+// codes: 3-9 per 2048-symbol chunk).  The chunk's symbols are renamed to
+// ids 0..D-1 (first occurrence order) with __match_any_sync; a chunk with
+// more than kBmMaxSyms distinct symbols is listed for the wide-cell pass
+// (encode.cu), which handles any alphabet.
+#include "common.cuh"
+
+namespace plzgpu {
+namespace {
+
+constexpr uint32_t kFull = 0xffffffffu;
+
+// x >> s and x << s with PTX clamping (s >= 32 gives 0).
+__device__ __forceinline__ uint32_t shr_clamp(uint32_t x, uint32_t s) {
+    uint32_t r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t s) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Issue the staging of chunk ck's bytes into raw: one TMA bulk copy (async,
+// completes on mbar) when the chunk is 16-byte granular, else a warp copy.
+// Waits first (bounded, ~4 s) for the chunk's H2D segment when the
+// pipelined host path is active; returns false if it never arrives.
+__device__ __forceinline__ bool stage_chunk(const EncodeArgs& a, uint64_t ck, int C, int S,
+                                            uint8_t* raw, uint64_t* mbar, uint32_t lane,
+                                            bool& async) {
+    const int n = (ck + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
+    const uint32_t nbytes = uint32_t(n) * S;
+    const uint8_t* src = a.in + ck * uint64_t(C) * S;
+    if (a.ready) {
+        uint32_t ok = 1;
+        if (lane == 0) {
+            const uint32_t* f = a.ready + ck / a.seg_chunks;
+            const long long t0 = clock64();
+            while (ld_acquire_sys(f) != a.epoch) {
+                __nanosleep(256);
+                if (clock64() - t0 > (1ll << 33)) {
+                    atomicExch(a.stalled, 1u);
+                    ok = 0;
+                    break;
+                }
+            }
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        if (!__shfl_sync(kFull, ok, 0)) return false;
+    }
+    async = a.bulk_ok && (nbytes & 15u) == 0;
+    if (async) {
+        fence_proxy_async_smem();  // earlier generic reads of raw before the TMA write
+        __syncwarp();
+        if (lane == 0) bulk_g2s(raw, src, nbytes, mbar);
+    } else {
+        __syncwarp();
+        for (uint32_t i = lane; i < nbytes; i += 32) raw[i] = src[i];
+        __syncwarp();
+    }
+    return true;
+}
+
+// Write 32 (or the final cnt) tokens held one per lane: lane l holds token
+// t0 + l as 0x80000000 | len | off << 8 (pointer) or its position (literal).
+// Payload offsets follow from popcounts (pointer 2 B, literal S B); literal
+// symbols come from the id table (lane d of `tab` holds id d's symbol).  The
+// flag word is the ballot of pointer lanes, bit-reversed within each byte
+// (MSB-first, encoder.cpp:33).
+template <int S>
+__device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32_t t0,
+                                             uint32_t& pl, uint32_t tab, const uint8_t* ids,
+                                             uint8_t* pay, uint32_t* fl32, uint32_t lane,
+                                             unsigned long long* hist) {
+    const bool valid = lane < cnt;
+    const bool isptr = valid && (tokv >> 31);
+    const uint32_t pm = __ballot_sync(kFull, isptr);
+    const uint32_t vm = cnt >= 32 ? kFull : ((1u << cnt) - 1u);
+    const uint32_t lm = lanemask_lt();
+    const uint32_t at = pl + 2u * __popc(pm & lm) + uint32_t(S) * __popc(vm & ~pm & lm);
+    const uint32_t id = (valid && !isptr) ? uint32_t(ids[tokv]) : 0u;
+    const uint32_t sym = __shfl_sync(kFull, tab, id);
+    if (valid) {
+        if (isptr) {
+            if constexpr (S == 1) {
+                pay[at] = uint8_t(tokv);
+                pay[at + 1] = uint8_t(tokv >> 8);
+            } else {
+                *reinterpret_cast<uint16_t*>(pay + at) = uint16_t(tokv);
+            }
+            if (hist) atomicAdd(&hist[tokv & 0xffu], 1ull);
+        } else {
+            if constexpr (S == 1) {
+                pay[at] = uint8_t(sym);
+            } else {
+                *reinterpret_cast<uint16_t*>(pay + at) = uint16_t(sym);
+                if constexpr (S == 4) *reinterpret_cast<uint16_t*>(pay + at + 2) = uint16_t(sym >> 16);
+            }
+        }
+    }
+    if (lane == 0) fl32[t0 >> 5] = __byte_perm(__brev(pm), 0u, 0x0123);
+    pl += 2u * __popc(pm) + uint32_t(S) * __popc(vm & ~pm);
+}
+
+template <int S, int NW>
+__global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs a) {
+    using T = typename Sym<S>::T;
+    constexpr int G = 32 / NW;
+    constexpr int LNW = NW == 1 ? 0 : NW == 2 ? 1 : NW == 4 ? 2 : 3;
+    extern __shared__ __align__(16) uint8_t smem[];
+
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    const int C = a.C, W = a.W;
+    const int RW = bm_row_words(C, W);
+    // [mbarrier 16][raw chunk, then its ids in place: C*S + 16][rows: (Dmax+1) x RW words]
+    uint8_t* base = smem + bm_warp_smem(C, S, W) * warp;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(base);
+    uint8_t* raw = base + 16;
+    uint8_t* ids = raw;
+    uint32_t* rows = reinterpret_cast<uint32_t*>(raw + size_t(C) * S + 16);
+
+    // row kBmMaxSyms stays all-zero: the id of "position n" (past the chunk)
+    for (int x = static_cast<int>(lane); x < RW; x += 32) rows[kBmMaxSyms * RW + x] = 0u;
+    if (lane == 0) mbar_init(mbar, 1);
+    __syncwarp();
+    uint32_t phase = 0;
+    unsigned long long warp_ptr = 0, warp_tok = 0;
+
+    const int grp = static_cast<int>(lane) >> LNW;  // step group
+    const int jw = static_cast<int>(lane) & (NW - 1);  // word of the candidate set
+    const int clg = 32 * (jw + 1) - W + grp;       // step-(k+grp) mask: ~0 >> max(clg + k, 0)
+    const int qc = 32 * NW - W + 32 * jw + grp;    // row bit of candidate word jw at step grp: p + qc + k
+    const int lbc = W - 32 * jw;                   // w >= 0  <=>  bit >= lbc - p
+    const uint32_t low = (1u << NW) - 1u;
+    const int Im1 = a.I - 1;
+    const uint32_t min_match = uint32_t(a.min_match);
+
+    for (;;) {
+        uint64_t ck = 0;
+        if (lane == 0) ck = atomicAdd(a.work, 1u);
+        ck = __shfl_sync(kFull, ck, 0);
+        if (ck >= a.n_chunks) break;
+        const int n = (ck + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
+        bool async = false;
+        if (!stage_chunk(a, ck, C, S, raw, mbar, lane, async)) break;
+        if (async) {
+            mbar_wait(mbar, phase);
+            phase ^= 1u;
+        }
+
+        // ---- ids (in place over the raw symbols: id i lands on byte i <= S*i,
+        // after word i/32 is read) and occurrence bitmaps, one 32-position word
+        // at a time: lanes holding equal symbols form one __match_any_sync
+        // group, whose mask IS that symbol's bitmap word.  Lane d of the warp
+        // keeps the symbol of id d (tab) for literal emission.
+        const T* rs = reinterpret_cast<const T*>(raw);
+        int D = 0;
+        uint32_t tab = 0;
+        bool ok = true;
+        for (int wi = 0; wi * 32 < n && ok; ++wi) {
+            const int i = wi * 32 + static_cast<int>(lane);
+            const bool valid = i < n;
+            const uint32_t vmask = __ballot_sync(kFull, valid);
+            const uint32_t v = valid ? uint32_t(rs[i]) : 0u;
+            const uint32_t same = __match_any_sync(kFull, v) & vmask;
+            const bool leader = valid && (__ffs(same) - 1 == static_cast<int>(lane));
+            uint32_t lead = __ballot_sync(kFull, leader);
+            uint32_t myid = 0;
+            while (lead) {
+                const int l = __ffs(lead) - 1;
+                lead &= lead - 1;
+                const uint32_t vl = __shfl_sync(kFull, v, l);
+                const uint32_t hit = __ballot_sync(kFull, static_cast<int>(lane) < D && tab == vl);
+                uint32_t id;
+                if (hit) {
+                    id = __ffs(hit) - 1;
+                } else {
+                    if (D == kBmMaxSyms) {
+                        ok = false;
+                        break;
+                    }
+                    id = D;
+                    if (static_cast<int>(lane) == D) tab = vl;
+                    ++D;
+                    uint32_t* row = rows + id * RW;
+                    for (int x = static_cast<int>(lane); x < RW; x += 32) row[x] = 0u;
+                }
+                if (valid && v == vl) myid = id;
+            }
+            __syncwarp();  // reads of the word and row zeroing before the stores
+            if (ok) {
+                if (leader) rows[myid * RW + NW + wi] = same;
+                if (valid) ids[i] = uint8_t(myid);
+            }
+        }
+        if (!ok) {  // too many distinct symbols: the wide-cell pass takes it
+            if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1u)] = uint32_t(ck);
+            __syncwarp();
+            continue;
+        }
+        if (lane == 0) ids[n] = uint8_t(kBmMaxSyms);
+        __syncwarp();
+
+        // ---- greedy walk (encoder.cpp:25-41); lane t % 32 holds token t
+        // until the batch of 32 is flushed straight into the chunk's slots
+        uint8_t* pay = a.pay_slots + ck * uint64_t(C) * S;
+        uint32_t* fl32 = reinterpret_cast<uint32_t*>(a.flag_slots + ck * uint64_t(C / 8));
+        int p = 0;
+        uint32_t t = 0, pl = 0, tokv = 0, nptr = 0;
+        while (p < n) {
+            uint32_t K = 0, off = 0;
+            if (p > 0 && (p & Im1) == 0) {
+                // bit b of word jw <-> candidate w = p - W + 32*jw + b
+                uint32_t A = shl_clamp(kFull, uint32_t(max(lbc - p, 0)));
+                uint32_t x, nz;
+                const uint8_t* idp = ids + p + grp;
+                const uint32_t* rq = rows + ((p + qc) >> 5);
+                int sh = (p + qc) & 31, k = 0, lim = n - p - grp;
+                for (;;) {
+                    // step k + grp: candidates whose symbol at w + k + grp equals x[p + k + grp]
+                    const uint32_t id = idp[min(k, lim)];
+                    const uint32_t* r = rq + id * RW;
+                    const uint32_t f = __funnelshift_r(r[0], r[1], uint32_t(sh));
+                    x = f & shr_clamp(kFull, uint32_t(max(clg + k, 0))) & A;
+#pragma unroll
+                    for (int d = 1; d < G; d <<= 1) x &= __shfl_up_sync(kFull, x, d * NW);
+                    nz = __ballot_sync(kFull, x != 0u);
+                    const uint32_t An = __shfl_sync(kFull, x, (G - 1) * NW + jw);
+                    if ((nz >> (32 - NW)) == 0u) break;  // the search ends in this round
+                    A = An;
+                    k += G;
+                    sh += G;
+                    rq += sh >> 5;
+                    sh &= 31;
+                }
+                // steps matched in the last round: groups with non-empty sets
+                const int e = (static_cast<int>(31 - __clz(nz)) + NW) >> LNW;  // nz == 0 -> 0
+                K = uint32_t(k + e);
+                if (K >= min_match) {
+                    // winner: lowest set bit of A_K (group e-1 of x, or A)
+                    const int l0 = e > 0 ? (e - 1) * NW : 0;
+                    const uint32_t bits = e > 0 ? (nz >> l0) & low : __ballot_sync(kFull, A != 0u) & low;
+                    const int js = __ffs(bits) - 1;
+                    const uint32_t wv = __shfl_sync(kFull, e > 0 ? x : A, l0 + js);
+                    off = uint32_t(W - (32 * js + __ffs(wv) - 1));
+                }
+            }
+            const bool ptr = K >= min_match;
+            if (lane == (t & 31u)) tokv = ptr ? (0x80000000u | K | (off << 8)) : uint32_t(p);
+            p += ptr ? static_cast<int>(K) : 1;
+            nptr += ptr ? 1u : 0u;
+            ++t;
+            if ((t & 31u) == 0)
+                flush_tokens<S>(tokv, 32u, t - 32u, pl, tab, ids, pay, fl32, lane, a.hist);
+        }
+        if (t & 31u) flush_tokens<S>(tokv, t & 31u, t & ~31u, pl, tab, ids, pay, fl32, lane, a.hist);
+        if (lane == 0) {
+            a.psize[ck] = pl;
+            a.fsize[ck] = (t + 7u) >> 3;
+        }
+        warp_ptr += nptr;
+        warp_tok += t;
+        __syncwarp();
+    }
+    if (lane == 0 && warp_tok) {
+        atomicAdd(&a.stats[0], warp_ptr);
+        atomicAdd(&a.stats[1], warp_tok - warp_ptr);
+    }
+}
+
+template <int S>
+const void* bitmatch_fn_s(int nw) {
+    switch (nw) {
+        case 1: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 1>);
+        case 2: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 2>);
+        case 4: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 4>);
+        default: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 8>);
+    }
+}
+
+const void* bitmatch_fn(int S, int W) {
+    const int nw = bm_nw(W);
+    if (S == 1) return bitmatch_fn_s<1>(nw);
+    if (S == 2) return bitmatch_fn_s<2>(nw);
+    return bitmatch_fn_s<4>(nw);
+}
+
+}  // namespace
+
+int bitmatch_ctas_per_sm(int S, int C, int W, int warps_per_cta) {
+    int blocks = 0;
+    const size_t smem = bm_warp_smem(C, S, W) * warps_per_cta;
+    const void* fn = bitmatch_fn(S, W);
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, warps_per_cta * 32, smem);
+    return blocks;
+}
+
+void launch_bitmatch(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = bm_warp_smem(a.C, S, a.W) * a.warps_per_cta;
+    const void* fn = bitmatch_fn(S, a.W);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    void* args[] = {const_cast<EncodeArgs*>(&a)};
+    cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
+}
+
+}  // namespace plzgpu

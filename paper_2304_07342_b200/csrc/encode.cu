@@ -256,113 +256,31 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
     return __reduce_max_sync(0xffffffffu, best);
 }
 
-// Dictionary cells (S in {2, 4}): one right-to-left pass over 32-position
-// words computes the equal-run lengths (ballot, as for wide cells) and renames
-// each symbol to its slot in the warp's 256-entry open-addressing table, so a
-// cell is (id8 | run8 << 8) and matching is the S = 1 code on ids (lcp only
-// compares symbols for equality; the renaming is a bijection on the chunk).
-// Lookups probe in parallel; the few new symbols are inserted one at a time
-// (serialised in the warp, no atomics).  Returns false if the chunk has more
-// than 256 distinct symbols.  Cells overwrite raw symbols in place: cell i's
-// bytes lie over raw positions >= i, which are already read.
+// Kernel I, wide-cell pass: chunks the bitmap pass (bitmatch.cu) left
+// because their alphabet exceeds kBmMaxSyms (from_list), or every chunk.
+// Cells keep (symbol, run) in 2S bytes, so any alphabet works.
 template <int S>
-__device__ __forceinline__ bool build_dict_cells(const uint8_t* raw8, uint16_t* cells,
-                                                 uint32_t* keys, uint32_t* occ, int n,
-                                                 uint32_t lane) {
-    using T = typename Sym<S>::T;
-    const T* raw = reinterpret_cast<const T*>(raw8);
-    if (lane < 8) occ[lane] = 0u;
-    __syncwarp();
-    uint32_t carry = 0, after = 0;  // run length / symbol at the next word's first position
-    for (int w = (n - 1) >> 5; w >= 0; --w) {
-        const int i = (w << 5) + static_cast<int>(lane);
-        const uint32_t v = i < n ? uint32_t(raw[i]) : 0u;
-        uint32_t nx = __shfl_down_sync(0xffffffffu, v, 1);
-        if (lane == 31) nx = after;
-        const bool eq = (i + 1 < n) && nx == v;
-        const uint32_t m = __ballot_sync(0xffffffffu, eq);
-        const uint32_t sh = m >> lane;
-        uint32_t r = sh == (0xffffffffu >> lane) ? (32u - lane) + carry
-                                                 : static_cast<uint32_t>(__ffs(~sh));
-        r = r < 255u ? r : 255u;
-        carry = __shfl_sync(0xffffffffu, r, 0);
-        after = __shfl_sync(0xffffffffu, v, 0);
-        uint32_t h = (v * 0x9E3779B1u) >> 24;
-        bool found = i >= n;
-        if (!found) {
-            for (int k = 0; k < 256; ++k) {
-                if (!((occ[h >> 5] >> (h & 31u)) & 1u)) break;  // free slot: not present
-                if (keys[h] == v) {
-                    found = true;
-                    break;
-                }
-                h = (h + 1u) & 255u;
-            }
-        }
-        uint32_t pend = __ballot_sync(0xffffffffu, !found);
-        while (pend) {
-            const int l = __ffs(pend) - 1;
-            const uint32_t sl = __shfl_sync(0xffffffffu, v, l);
-            const uint32_t h0 = (sl * 0x9E3779B1u) >> 24;
-            uint32_t slot = 256u;
-            for (uint32_t b = 0; b < 256u; b += 32u) {
-                const uint32_t q = (h0 + b + lane) & 255u;
-                const uint32_t fm = __ballot_sync(0xffffffffu, !((occ[q >> 5] >> (q & 31u)) & 1u));
-                if (fm) {
-                    slot = (h0 + b + uint32_t(__ffs(fm) - 1)) & 255u;
-                    break;
-                }
-            }
-            if (slot == 256u) return false;  // > 256 distinct symbols (warp-uniform)
-            if (lane == 0) {
-                keys[slot] = sl;
-                occ[slot >> 5] |= 1u << (slot & 31u);
-            }
-            __syncwarp();
-            if (!found && v == sl) {
-                h = slot;
-                found = true;
-            }
-            pend = __ballot_sync(0xffffffffu, !found);
-        }
-        if (i < n) cells[i] = uint16_t(h | (r << 8));
-    }
-    __syncwarp();
-    return true;
-}
-
-// Kernel I.  kDict (S in {2, 4}): dictionary cells, matching with the S = 1
-// code; chunks with > 256 distinct symbols are listed for the wide pass
-// (kDict = false, from_list), which keeps (symbol, run) cells of 2S bytes.
-template <int S, bool kDict>
 __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     using T = typename Sym<S>::T;
-    constexpr int MS = kDict ? 1 : S;  // width the matcher sees
-    using Cell = typename Sym<MS>::Cell;
+    using Cell = typename Sym<S>::Cell;
     extern __shared__ __align__(16) uint8_t smem[];
 
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     const int C = a.C;
-    const size_t per_warp = kDict ? encode_dict_warp_smem(C, S) : encode_warp_smem(C, S);
-    const size_t kHead = kDict ? encode_dict_head(C, S) : size_t(kEncodeHeadPerS) * S;
-    uint8_t* base = smem + per_warp * warp;
+    constexpr size_t kHead = size_t(kEncodeHeadPerS) * S;
+    uint8_t* base = smem + encode_warp_smem(C, S) * warp;
     // [payload head: kHead B][cells: C x sizeof(Cell)][flags: C/8 B][list][mbarrier]
-    // (+ kDict: [keys: 256 x u32][occupancy: 8 x u32]).
     // Payload byte b is stored at head[b]: beyond kHead it runs on into the
     // cell array.  It is written at a step p with b < S*(p+1) <= kHead +
     // sizeof(Cell)*(p-W), i.e. over cells left of the window that are never
-    // read again (see encode_warp_smem / encode_dict_head).
+    // read again (see encode_warp_smem).
     uint8_t* head = base;
     Cell* cells = reinterpret_cast<Cell*>(base + kHead);
-    // raw stage: the upper half of wide cells; dictionary S = 2 in place,
-    // S = 4 over head + cells (converted right to left)
-    uint8_t* raw8 = kDict ? (S == 2 ? base + kHead : base) : base + kHead + size_t(C) * S;
+    uint8_t* raw8 = base + kHead + size_t(C) * S;  // raw stage: the upper half of the cells
     uint8_t* flg = base + kHead + size_t(C) * sizeof(Cell);      // C/8 bytes
     uint8_t* list = flg + C / 8;                                  // 256 B continuation list
     uint64_t* mbar = reinterpret_cast<uint64_t*>(list + 256);     // 8B aligned
-    uint32_t* keys = reinterpret_cast<uint32_t*>(list + 256 + 16);  // kDict: id -> symbol
-    uint32_t* occ = keys + 256;
 
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
@@ -373,7 +291,7 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         uint64_t g = 0;
         if (lane == 0) {
             const uint32_t idx = atomicAdd(a.work, 1u);
-            if (kDict || !a.from_list) g = idx;
+            if (!a.from_list) g = idx;
             else g = idx < *a.fb_count ? a.fb_list[idx] : a.n_chunks;
         }
         g = __shfl_sync(0xffffffffu, g, 0);
@@ -414,13 +332,7 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
             __syncwarp();
         }
 
-        if constexpr (kDict) {
-            if (!build_dict_cells<S>(raw8, reinterpret_cast<uint16_t*>(cells), keys, occ, n, lane)) {
-                if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1u)] = uint32_t(g);
-                __syncwarp();
-                continue;
-            }
-        } else {
+        {
             // ---- symbols into cells, in place, left to right (a word's writes
             // only clobber raw symbols that are already read)
             const T* raw = reinterpret_cast<const T*>(raw8);
@@ -460,13 +372,11 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         uint32_t t = 0, pl = 0, fw = 0, nptr = 0;
         while (p < n) {
             uint32_t key = 0;
-            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<MS>(cells, p, n, W, lane, list);
+            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<S>(cells, p, n, W, lane, list);
             const uint32_t k = key >> 8, o = key & 255u;
             const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
             if (lane == 0) {
-                T v;
-                if constexpr (kDict) v = T(keys[cells[p] & 0xffu]);
-                else v = cell_sym<S>(cells[p]);
+                const T v = cell_sym<S>(cells[p]);
                 if constexpr (S == 1) {
                     head[pl] = ptr ? uint8_t(k) : uint8_t(v);
                     if (ptr) head[pl + 1] = uint8_t(o);
@@ -606,36 +516,27 @@ void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, 
     }
 }
 
-template <int S, bool D>
-const void* encode_fn() {
-    return reinterpret_cast<const void*>(plz_encode_kernel<S, D>);
+const void* encode_kernel_for(int S) {
+    if (S == 1) return reinterpret_cast<const void*>(plz_encode_kernel<1>);
+    if (S == 2) return reinterpret_cast<const void*>(plz_encode_kernel<2>);
+    return reinterpret_cast<const void*>(plz_encode_kernel<4>);
 }
 
-const void* encode_kernel_for(int S, bool dict) {
-    if (S == 1) return encode_fn<1, false>();
-    if (S == 2) return dict ? encode_fn<2, true>() : encode_fn<2, false>();
-    return dict ? encode_fn<4, true>() : encode_fn<4, false>();
-}
-
-int encode_ctas_per_sm(int S, int C, int warps_per_cta, bool dict) {
-    dict = dict && S > 1;
+int encode_ctas_per_sm(int S, int C, int warps_per_cta) {
     int blocks = 0;
-    const size_t smem = (dict ? encode_dict_warp_smem(C, S) : encode_warp_smem(C, S)) * warps_per_cta;
-    const void* fn = encode_kernel_for(S, dict);
+    const size_t smem = encode_warp_smem(C, S) * warps_per_cta;
+    const void* fn = encode_kernel_for(S);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, warps_per_cta * 32, smem);
     return blocks;
 }
 
-void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st, bool dict) {
-    dict = dict && S > 1;
-    const size_t smem =
-        (dict ? encode_dict_warp_smem(a.C, S) : encode_warp_smem(a.C, S)) * a.warps_per_cta;
-    const dim3 block(a.warps_per_cta * 32);
-    const void* fn = encode_kernel_for(S, dict);
+void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = encode_warp_smem(a.C, S) * a.warps_per_cta;
+    const void* fn = encode_kernel_for(S);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     void* args[] = {const_cast<EncodeArgs*>(&a)};
-    cudaLaunchKernel(fn, dim3(grid), block, args, smem, st);
+    cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
 }  // namespace plzgpu

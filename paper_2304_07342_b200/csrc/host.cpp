@@ -195,9 +195,9 @@ struct plzgpu_ctx {
     int last_launches = 0;
     LastOp last_op = OP_NONE;
     DecodeArgs last_decode{};
-    int enc_wpc[320] = {};   // launch shape cache per (S, C, dictionary)
-    int enc_ctas[320] = {};
-    DevBuf fb;               // chunks the dictionary pass left to the wide pass
+    int enc_wpc[800] = {};   // launch shape cache per (pass, S, C)
+    int enc_ctas[800] = {};
+    DevBuf fb;               // chunks the bitmap pass left to the wide pass
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
     cudaStream_t copy_stream = nullptr;
@@ -221,23 +221,29 @@ cudaStream_t pick(plzgpu_ctx*, void* s) { return static_cast<cudaStream_t>(s); }
 
 Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
 
-// Launch shape of Kernel I for (S, C, dictionary), cached per context: warps
-// per CTA that maximise resident warps per SM (shared-memory limited).
-void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, bool dict, int* wpc_out,
+// Launch shape of Kernel I (bitmap or wide pass) for (S, C, W), cached per
+// context: warps per CTA that maximise resident warps per SM (shared-memory
+// limited).
+void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, bool bitmap, int* wpc_out,
                   int* per_sm_out) {
-    const int key = (dict ? 160 : 0) + p.symbol_width * 32 +
-                    (__builtin_ctz(unsigned(p.chunk_size)) - 10);
+    const int pass = bitmap ? 1 + __builtin_ctz(unsigned(bm_nw(p.window))) : 0;  // 0..4
+    const int key = pass * 160 + p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
     int& wpc = c->enc_wpc[key];
     int& per_sm = c->enc_ctas[key];
     if (wpc == 0) {
         int best_warps = 0;
-        for (int cand = 1; cand <= 16; ++cand) {
-            const int ctas = encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand, dict);
+        for (int cand = 1; cand <= (bitmap ? kBmMaxThreads / 32 : 16); ++cand) {
+            const int ctas = bitmap ? bitmatch_ctas_per_sm(p.symbol_width, p.chunk_size, p.window, cand)
+                                    : encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
             if (ctas * cand > best_warps) {
                 best_warps = ctas * cand;
                 wpc = cand;
                 per_sm = ctas;
             }
+        }
+        if (best_warps == 0) {  // does not fit (huge chunks): one warp, one CTA
+            wpc = 1;
+            per_sm = 0;
         }
     }
     *wpc_out = wpc;
@@ -293,32 +299,31 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
     e.hist = c->enc_hist;
-    // S in {2, 4}: dictionary pass, then the wide pass over the chunks it left
-    const bool dict = p.symbol_width > 1;
-    if (dict) {
+    // bitmap pass over every chunk, then the wide pass over the chunks whose
+    // alphabet it could not hold
+    int wpc = 1, per_sm = 1;
+    encode_shape(c, p, true, &wpc, &per_sm);
+    const bool bitmap = per_sm > 0;
+    if (bitmap) {
         CK(c->fb.ensure(G * 4 + 16));
         e.fb_list = c->fb.as<uint32_t>();
         e.fb_count = &m->work[4];
-    }
-    int wpc = 1, per_sm = 1;
-    encode_shape(c, p, dict, &wpc, &per_sm);
-    e.warps_per_cta = wpc;
-    launch_encode(p.symbol_width, e, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
-                                                          (G + wpc - 1) / wpc)),
-                  st, dict);
-    ++*launches;
-    if (dict) {
-        EncodeArgs f = e;
-        f.from_list = 1;
-        f.work = &m->work[5];
-        f.ready = nullptr;  // every segment has landed once the dictionary pass ends
-        encode_shape(c, p, false, &wpc, &per_sm);
-        f.warps_per_cta = wpc;
-        launch_encode(p.symbol_width, f, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
-                                                              (G + wpc - 1) / wpc)),
-                      st, false);
+        e.warps_per_cta = wpc;
+        launch_bitmatch(p.symbol_width, e, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
+                                                                (G + wpc - 1) / wpc)),
+                        st);
         ++*launches;
     }
+    EncodeArgs f = e;
+    f.from_list = bitmap ? 1 : 0;
+    f.work = &m->work[5];
+    if (bitmap) f.ready = nullptr;  // every segment has landed once the bitmap pass ends
+    encode_shape(c, p, false, &wpc, &per_sm);
+    f.warps_per_cta = wpc;
+    launch_encode(p.symbol_width, f, int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1),
+                                                          (G + wpc - 1) / wpc)),
+                  st);
+    ++*launches;
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
     ScanArgs sa{};

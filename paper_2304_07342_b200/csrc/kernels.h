@@ -1,6 +1,7 @@
 // kernels.h — host-visible launchers and argument blocks of the sm_100a kernels.
 //
-//   Kernel I   plz_encode_kernel<S>     match + greedy token walk + encode, one warp per chunk
+//   Kernel I   plz_bitmatch_kernel<S,NW> match + greedy token walk + encode, one warp per chunk
+//              plz_encode_kernel<S>     the same for chunks with a large alphabet (wide cells)
 //   Kernel II  plz_scan_kernel          decoupled look-back exclusive scan of (payload, flag) sizes
 //   Kernel III plz_assemble_kernel      tables + flag/payload streams into the image (128-bit stores)
 //              plz_headers_kernel       container headers, last table entries, tails, image length
@@ -44,19 +45,19 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
     return (b + 15) & ~size_t(15);
 }
 
-// Dictionary layout of Kernel I for S in {2, 4} (plz_encode_kernel<S, true>):
-// the chunk's symbols are renamed to 8-bit ids (slot of a 256-entry hash
-// table), so cells are 16-bit (id, run) and matching runs the S = 1 code.
-//   [payload head: H][cells: C x 2 B][flags: C/8][list: 256][mbar: 16]
-//   [keys: 256 x u32][occupancy: 8 x u32]
-// H >= S*(p+1) - 2*(p-W) for every step p: 2W+2 for S = 2, 2C+2W+4 for S = 4
-// (S = 4 also lands its 4C raw bytes over head + cells and converts them
-// right to left).
-__host__ __device__ inline size_t encode_dict_head(int C, int S) {
-    return S == 2 ? 512 : size_t(2) * C + 512;
-}
-__host__ __device__ inline size_t encode_dict_warp_smem(int C, int S) {
-    size_t b = encode_dict_head(C, S) + size_t(C) * 2 + size_t(C) / 8 + 256 + 16 + 1024 + 32;
+// Bitmap pass of Kernel I (bitmatch.cu): chunks with at most kBmMaxSyms
+// distinct symbols.  Per warp:
+//   [mbarrier 16][raw chunk (TMA target), then its ids in place: C*S + 16]
+//   [occurrence rows: (kBmMaxSyms + 1) x RW words]
+// A row is the chunk's C-bit occurrence bitmap of one symbol with NW zero
+// words in front (windows reaching before position 0) and NW + 1 behind;
+// row kBmMaxSyms stays zero (the id of position n).
+constexpr int kBmMaxSyms = 16;
+constexpr int kBmMaxThreads = 128;  // CTA size bound (registers: up to 255 per thread)
+__host__ __device__ inline int bm_nw(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8; }
+__host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 1; }
+__host__ __device__ inline size_t bm_warp_smem(int C, int S, int W) {
+    size_t b = 16 + size_t(C) * S + 16 + size_t(kBmMaxSyms + 1) * bm_row_words(C, W) * 4;
     return (b + 15) & ~size_t(15);
 }
 
@@ -80,18 +81,21 @@ struct EncodeArgs {
     uint32_t seg_chunks;
     uint32_t* stalled;           // set if a segment never arrives (bounded wait)
     unsigned long long* hist;    // optional: selected pointer lengths [256]
-    // dictionary pass: chunks with > 256 distinct symbols are appended to
+    // bitmap pass: chunks with > kBmMaxSyms distinct symbols are appended to
     // fb_list; the wide pass then takes its chunks from fb_list[0..*fb_count)
     uint32_t* fb_list;
     uint32_t* fb_count;
     int from_list;               // wide pass: iterate fb_list instead of 0..n_chunks
 };
-// dict: the 8-bit dictionary kernel (S in {2, 4}); otherwise the wide-cell kernel
-void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st, bool dict = false);
+// the wide-cell kernel (any alphabet); from_list selects the fallback mode
+void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+// the bitmap kernel (bitmatch.cu): chunks with <= kBmMaxSyms distinct symbols
+void launch_bitmatch(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+int bitmatch_ctas_per_sm(int S, int C, int W, int warps_per_cta);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
 void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
                         unsigned long long* raw_hist, cudaStream_t st);
-int encode_ctas_per_sm(int S, int C, int warps_per_cta, bool dict = false);
+int encode_ctas_per_sm(int S, int C, int warps_per_cta);
 
 struct ScanArgs {
     const uint32_t* psize;
