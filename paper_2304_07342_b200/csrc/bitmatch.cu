@@ -29,9 +29,9 @@
 //
 // Occurrence bitmaps need one row per distinct symbol of the chunk (quant
 // codes: 3-9 per 2048-symbol chunk).  The chunk's symbols are renamed to
-// ids 0..D-1 (first occurrence order) with __match_any_sync; a chunk with
-// more than kBmMaxSyms distinct symbols is listed for the wide-cell pass
-// (encode.cu), which handles any alphabet.
+// ids 0..D-1 (first occurrence order); a chunk with more than kBmMaxSyms
+// distinct symbols is listed for the wide-cell pass (encode.cu), which
+// handles any alphabet.
 #include "common.cuh"
 
 namespace plzgpu {
@@ -137,9 +137,86 @@ __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32
     pl += 2u * __popc(pm) + uint32_t(S) * __popc(vm & ~pm);
 }
 
+// Pass 1: rename the chunk's symbols to ids 0..D-1 (first-occurrence order)
+// in place (id i lands on byte i <= S*i, after word i/32 is read), through a
+// small open-addressing table; lane d of the warp keeps id d's symbol in tab.
+// New symbols (at most kBmMaxSyms per chunk, so rare) are inserted one
+// distinct value at a time.  Returns false when the chunk has more than
+// kBmMaxSyms distinct symbols.
+template <int S>
+__device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, uint32_t lane,
+                                               int& D, uint32_t& tab) {
+    using T = typename Sym<S>::T;
+    constexpr uint32_t kEmpty = 0xffffffffu;
+    tbl[lane] = make_uint2(0u, kEmpty);  // kBmHash == 32 entries
+    __syncwarp();
+    const T* rs = reinterpret_cast<const T*>(raw);
+    D = 0;
+    tab = 0;
+    for (int wi = 0; wi * 32 < n; ++wi) {
+        const int i = wi * 32 + static_cast<int>(lane);
+        const bool valid = i < n;
+        const uint32_t v = valid ? uint32_t(rs[i]) : 0u;
+        uint32_t h = (v * 0x9E3779B1u) >> 27, id = kEmpty;
+        if (valid) {
+            for (;;) {
+                const uint2 e = tbl[h];
+                if (e.y == kEmpty) break;
+                if (e.x == v) {
+                    id = e.y;
+                    break;
+                }
+                h = (h + 1u) & (kBmHash - 1);
+            }
+        }
+        const bool missing = valid && id == kEmpty;
+        if (__any_sync(kFull, missing)) {
+            const uint32_t same = __match_any_sync(kFull, v) & __ballot_sync(kFull, missing);
+            uint32_t lead = __ballot_sync(kFull, missing && __ffs(same) - 1 == static_cast<int>(lane));
+            while (lead) {
+                const int l = __ffs(lead) - 1;
+                lead &= lead - 1;
+                const uint32_t vl = __shfl_sync(kFull, v, l);
+                if (D == kBmMaxSyms) return false;
+                if (lane == 0) {
+                    uint32_t hh = (vl * 0x9E3779B1u) >> 27;
+                    while (tbl[hh].y != kEmpty) hh = (hh + 1u) & (kBmHash - 1);
+                    tbl[hh] = make_uint2(vl, uint32_t(D));
+                }
+                if (static_cast<int>(lane) == D) tab = vl;
+                if (missing && v == vl) id = uint32_t(D);
+                ++D;
+                __syncwarp();
+            }
+        }
+        __syncwarp();  // every lane has read word wi before the in-place stores
+        if (valid) raw[i] = uint8_t(id);
+    }
+    __syncwarp();
+    return true;
+}
+
+// Pass 2: occurrence rows from the ids.  Lanes holding equal ids form one
+// __match_any_sync group, whose mask IS that id's bitmap word.  Rows 0..D
+// are cleared first (row D is the all-zero row of position n).
+template <int NW>
+__device__ __forceinline__ void build_rows(uint8_t* ids, int n, int D, uint32_t* rows, int RW,
+                                           uint32_t lane) {
+    for (int x = static_cast<int>(lane); x < (D + 1) * RW; x += 32) rows[x] = 0u;
+    __syncwarp();
+    for (int wi = 0; wi * 32 < n; ++wi) {
+        const int i = wi * 32 + static_cast<int>(lane);
+        const bool valid = i < n;
+        const uint32_t id = valid ? uint32_t(ids[i]) : 0xffu;
+        const uint32_t same = __match_any_sync(kFull, id);
+        if (valid && __ffs(same) - 1 == static_cast<int>(lane)) rows[id * RW + NW + wi] = same;
+    }
+    if (lane == 0) ids[n] = uint8_t(D);
+    __syncwarp();
+}
+
 template <int S, int NW>
 __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs a) {
-    using T = typename Sym<S>::T;
     constexpr int G = 32 / NW;
     constexpr int LNW = NW == 1 ? 0 : NW == 2 ? 1 : NW == 4 ? 2 : 3;
     extern __shared__ __align__(16) uint8_t smem[];
@@ -148,15 +225,14 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     const uint32_t warp = threadIdx.x >> 5;
     const int C = a.C, W = a.W;
     const int RW = bm_row_words(C, W);
-    // [mbarrier 16][raw chunk, then its ids in place: C*S + 16][rows: (Dmax+1) x RW words]
+    // [mbarrier 16][hash table][region: raw chunk -> ids [0, C) + rows at C]
     uint8_t* base = smem + bm_warp_smem(C, S, W) * warp;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base);
-    uint8_t* raw = base + 16;
+    uint2* tbl = reinterpret_cast<uint2*>(base + 16);
+    uint8_t* raw = base + 16 + kBmHash * 8;
     uint8_t* ids = raw;
-    uint32_t* rows = reinterpret_cast<uint32_t*>(raw + size_t(C) * S + 16);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(raw + C);
 
-    // row kBmMaxSyms stays all-zero: the id of "position n" (past the chunk)
-    for (int x = static_cast<int>(lane); x < RW; x += 32) rows[kBmMaxSyms * RW + x] = 0u;
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
     uint32_t phase = 0;
@@ -167,7 +243,6 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     const int clg = 32 * (jw + 1) - W + grp;       // step-(k+grp) mask: ~0 >> max(clg + k, 0)
     const int qc = 32 * NW - W + 32 * jw + grp;    // row bit of candidate word jw at step grp: p + qc + k
     const int lbc = W - 32 * jw;                   // w >= 0  <=>  bit >= lbc - p
-    const uint32_t low = (1u << NW) - 1u;
     const int Im1 = a.I - 1;
     const uint32_t min_match = uint32_t(a.min_match);
 
@@ -184,58 +259,15 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
             phase ^= 1u;
         }
 
-        // ---- ids (in place over the raw symbols: id i lands on byte i <= S*i,
-        // after word i/32 is read) and occurrence bitmaps, one 32-position word
-        // at a time: lanes holding equal symbols form one __match_any_sync
-        // group, whose mask IS that symbol's bitmap word.  Lane d of the warp
-        // keeps the symbol of id d (tab) for literal emission.
-        const T* rs = reinterpret_cast<const T*>(raw);
-        int D = 0;
-        uint32_t tab = 0;
-        bool ok = true;
-        for (int wi = 0; wi * 32 < n && ok; ++wi) {
-            const int i = wi * 32 + static_cast<int>(lane);
-            const bool valid = i < n;
-            const uint32_t vmask = __ballot_sync(kFull, valid);
-            const uint32_t v = valid ? uint32_t(rs[i]) : 0u;
-            const uint32_t same = __match_any_sync(kFull, v) & vmask;
-            const bool leader = valid && (__ffs(same) - 1 == static_cast<int>(lane));
-            uint32_t lead = __ballot_sync(kFull, leader);
-            uint32_t myid = 0;
-            while (lead) {
-                const int l = __ffs(lead) - 1;
-                lead &= lead - 1;
-                const uint32_t vl = __shfl_sync(kFull, v, l);
-                const uint32_t hit = __ballot_sync(kFull, static_cast<int>(lane) < D && tab == vl);
-                uint32_t id;
-                if (hit) {
-                    id = __ffs(hit) - 1;
-                } else {
-                    if (D == kBmMaxSyms) {
-                        ok = false;
-                        break;
-                    }
-                    id = D;
-                    if (static_cast<int>(lane) == D) tab = vl;
-                    ++D;
-                    uint32_t* row = rows + id * RW;
-                    for (int x = static_cast<int>(lane); x < RW; x += 32) row[x] = 0u;
-                }
-                if (valid && v == vl) myid = id;
-            }
-            __syncwarp();  // reads of the word and row zeroing before the stores
-            if (ok) {
-                if (leader) rows[myid * RW + NW + wi] = same;
-                if (valid) ids[i] = uint8_t(myid);
-            }
-        }
-        if (!ok) {  // too many distinct symbols: the wide-cell pass takes it
+        int D;
+        uint32_t tab;
+        if (!rename_symbols<S>(raw, n, tbl, lane, D, tab)) {
+            // too many distinct symbols: the wide-cell pass takes this chunk
             if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1u)] = uint32_t(ck);
             __syncwarp();
             continue;
         }
-        if (lane == 0) ids[n] = uint8_t(kBmMaxSyms);
-        __syncwarp();
+        build_rows<NW>(ids, n, D, rows, RW, lane);
 
         // ---- greedy walk (encoder.cpp:25-41); lane t % 32 holds token t
         // until the batch of 32 is flushed straight into the chunk's slots
@@ -249,14 +281,23 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
                 // bit b of word jw <-> candidate w = p - W + 32*jw + b
                 uint32_t A = shl_clamp(kFull, uint32_t(max(lbc - p, 0)));
                 uint32_t x, nz;
+                // step k + grp reads id x[p + k + grp] (clamped to position
+                // n, the zero row) and the row words at bit p + qc + k; the
+                // next round's loads are issued before this round's shuffles
                 const uint8_t* idp = ids + p + grp;
+                const int lim = n - p - grp;
                 const uint32_t* rq = rows + ((p + qc) >> 5);
-                int sh = (p + qc) & 31, k = 0, lim = n - p - grp;
+                int sh = (p + qc) & 31, k = 0;
+                const uint32_t* r = rq + uint32_t(idp[min(0, lim)]) * RW;
+                uint32_t lo = r[0], hi = r[1];
+                uint32_t idn = idp[min(G, lim)];
                 for (;;) {
-                    // step k + grp: candidates whose symbol at w + k + grp equals x[p + k + grp]
-                    const uint32_t id = idp[min(k, lim)];
-                    const uint32_t* r = rq + id * RW;
-                    const uint32_t f = __funnelshift_r(r[0], r[1], uint32_t(sh));
+                    const int shn = sh + G;
+                    const uint32_t* rqn = rq + (shn >> 5);
+                    const uint32_t* rn = rqn + idn * RW;
+                    const uint32_t lon = rn[0], hin = rn[1];
+                    idn = idp[min(k + 2 * G, lim)];
+                    const uint32_t f = __funnelshift_r(lo, hi, uint32_t(sh));
                     x = f & shr_clamp(kFull, uint32_t(max(clg + k, 0))) & A;
 #pragma unroll
                     for (int d = 1; d < G; d <<= 1) x &= __shfl_up_sync(kFull, x, d * NW);
@@ -265,20 +306,21 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
                     if ((nz >> (32 - NW)) == 0u) break;  // the search ends in this round
                     A = An;
                     k += G;
-                    sh += G;
-                    rq += sh >> 5;
-                    sh &= 31;
+                    sh = shn & 31;
+                    rq = rqn;
+                    lo = lon;
+                    hi = hin;
                 }
                 // steps matched in the last round: groups with non-empty sets
                 const int e = (static_cast<int>(31 - __clz(nz)) + NW) >> LNW;  // nz == 0 -> 0
                 K = uint32_t(k + e);
                 if (K >= min_match) {
                     // winner: lowest set bit of A_K (group e-1 of x, or A)
-                    const int l0 = e > 0 ? (e - 1) * NW : 0;
-                    const uint32_t bits = e > 0 ? (nz >> l0) & low : __ballot_sync(kFull, A != 0u) & low;
-                    const int js = __ffs(bits) - 1;
-                    const uint32_t wv = __shfl_sync(kFull, e > 0 ? x : A, l0 + js);
-                    off = uint32_t(W - (32 * js + __ffs(wv) - 1));
+                    const uint32_t val = e > 0 ? x : A;
+                    const int gsel = e > 0 ? e - 1 : 0;
+                    const uint32_t c = (grp == gsel && val != 0u)
+                                           ? uint32_t(32 * jw + __ffs(val) - 1) : kFull;
+                    off = uint32_t(W) - __reduce_min_sync(kFull, c);
                 }
             }
             const bool ptr = K >= min_match;

@@ -47,17 +47,27 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 
 // Bitmap pass of Kernel I (bitmatch.cu): chunks with at most kBmMaxSyms
 // distinct symbols.  Per warp:
-//   [mbarrier 16][raw chunk (TMA target), then its ids in place: C*S + 16]
-//   [occurrence rows: (kBmMaxSyms + 1) x RW words]
-// A row is the chunk's C-bit occurrence bitmap of one symbol with NW zero
-// words in front (windows reaching before position 0) and NW + 1 behind;
-// row kBmMaxSyms stays zero (the id of position n).
+//   [mbarrier 16][id hash table: kBmHash x {key, id} u32 pairs]
+//   [region: max(C*S, C + rows) + 16 bytes]
+// The region first holds the raw chunk (TMA target); pass 1 renames the
+// symbols to ids in place (bytes [0, C)); pass 2 builds the occurrence rows
+// at byte C, over the raw bytes pass 1 has consumed.  A row is the chunk's
+// C-bit occurrence bitmap of one id with NW zero words in front (windows
+// reaching before position 0) and NW + 3 behind (the search's one-round
+// look-ahead); row D (one past the chunk's last id) is all zero and is the
+// id of position n.
 constexpr int kBmMaxSyms = 16;
-constexpr int kBmMaxThreads = 128;  // CTA size bound (registers: up to 255 per thread)
+constexpr int kBmHash = 32;          // open addressing, load factor <= 1/2
+constexpr int kBmMaxThreads = 128;   // CTA size bound (registers: up to 255 per thread)
 __host__ __device__ inline int bm_nw(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8; }
-__host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 1; }
+__host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 3; }
+__host__ __device__ inline size_t bm_region(int C, int S, int W) {
+    const size_t raw = size_t(C) * S;
+    const size_t rows = size_t(C) + size_t(kBmMaxSyms + 1) * bm_row_words(C, W) * 4;
+    return (raw > rows ? raw : rows) + 16;
+}
 __host__ __device__ inline size_t bm_warp_smem(int C, int S, int W) {
-    size_t b = 16 + size_t(C) * S + 16 + size_t(kBmMaxSyms + 1) * bm_row_words(C, W) * 4;
+    const size_t b = 16 + size_t(kBmHash) * 8 + bm_region(C, S, W);
     return (b + 15) & ~size_t(15);
 }
 
