@@ -14,7 +14,7 @@ needed between steps.
 value      = compress GB/s of input bytes, whole job (sum over ranks / max time)
 e2e        = the same through the public C-ABI call with HOST buffers (pinned
              input H2D + image D2H inside the timed region)
-roofline   = Kernel I (plz_encode_kernel, the dominant kernel): algorithmic
+roofline   = Kernel I (plz_bitmatch_kernel, the dominant kernel): algorithmic
              bytes (input read + staged tokens written) / its CUDA-event time
 cpu_baseline = oracle/_ref (the reference library) on this host's cores
 
@@ -73,52 +73,84 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region.
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    Polls NVML (nvidia_ml_py) from a thread every 2 ms, so even a timed region
+    of a few tens of milliseconds gets samples; falls back to `nvidia-smi -lms`
+    when NVML is unavailable.  __enter__ returns once the first sample is in."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self._stop = None
+
+    def _poll_nvml(self, started):
+        import pynvml as N
+
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = [(name, getattr(N, attr)) for name, attr in self.REASONS]
+        while True:
+            sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append((float(sm), float(mx), [n for n, b in bits if r & b]))
+            started.set()
+            if self._stop.wait(0.002):
+                break
+        N.nvmlShutdown()
+
+    def _poll_smi(self, started):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_power_cap")
+        proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
+                                 "--format=csv,noheader,nounits", "-lms", "20"],
+                                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        names = [n for n, _ in self.REASONS]
+        for line in proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                self.samples.append((float(parts[0]), float(parts[1]),
+                                     [n for n, v in zip(names, parts[2:]) if v.lower().startswith("active")]))
+            except (ValueError, IndexError):
+                continue
+            started.set()
+            if self._stop.is_set():
+                break
+        proc.terminate()
 
     def __enter__(self):
+        import threading
+
+        self._stop = threading.Event()
+        started = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+            import pynvml  # noqa: F401
+            target = self._poll_nvml
+        except ImportError:
+            target = self._poll_smi
+        self._thread = threading.Thread(target=target, args=(started,), daemon=True)
+        self._thread.start()
+        started.wait(5.0)
+        self.samples.clear()  # keep only samples taken inside the region
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc:
-            time.sleep(0.12)
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-                self.lines = [l for l in out.splitlines() if l.strip()]
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        self._thread.join(timeout=5.0)
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            parts = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except (ValueError, IndexError):
-                continue
-            for n, v in zip(names, parts[2:]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
+        sm = [s[0] for s in self.samples]
+        mx = max((s[1] for s in self.samples), default=0)
+        reasons = sorted({r for s in self.samples for r in s[2]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": reasons, "samples": len(sm)}
 
 
 # ----------------------------------------------------------- reference arm
@@ -370,7 +402,7 @@ def run_b200(args):
 
     total_in = n * world
     peak, peak_kind = load_peaks()
-    prof = ncu_profile_facts("plz_encode_kernel")
+    prof = ncu_profile_facts("plz_bitmatch_kernel")
     enc_bytes = n + n_img  # input read + staged tokens written (~ image)
     achieved = enc_bytes / (enc_ms * 1e-3) / 1e9
     line = {
@@ -400,7 +432,7 @@ def run_b200(args):
                 "matches_device_image": e2e_ok,
                 "decompress": {"value": total_in / (e2e_d_ms * 1e-3) / 1e9, "unit": "GB/s",
                                "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n}},
-        "roofline": {"kernel": "plz_encode_kernel (Kernel I)", "bound": "hbm",
+        "roofline": {"kernel": "plz_bitmatch_kernel (Kernel I, bitmap pass)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,
                      "traffic": prof["dram_bytes"] if prof else None,

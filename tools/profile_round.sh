@@ -8,7 +8,7 @@ timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$R.json 2> 
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ -c 400 --csv \
     --log-file gpurun_out/launches_$R.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-for k in plz_encode plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
+for k in plz_bitmatch plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/prof_${k}_$R python tools/probe.py c2 1 > /dev/null 2>&1
 done
