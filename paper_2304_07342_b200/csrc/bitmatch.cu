@@ -55,6 +55,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
     return r;
 }
+// Shared-memory loads by 32-bit shared-window address (the search keeps its
+// cursors as plain integers; volatile keeps them ordered with the warp's
+// other shared-memory traffic).
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
 
 // Issue the staging of chunk ck's bytes into raw: one TMA bulk copy (async,
 // completes on mbar) when the chunk is 16-byte granular, else a warp copy.
@@ -104,7 +117,8 @@ __device__ __forceinline__ bool stage_chunk(const EncodeArgs& a, uint64_t ck, in
 // (MSB-first, encoder.cpp:33).
 template <int S>
 __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32_t t0,
-                                             uint32_t& pl, uint32_t tab, const uint8_t* ids,
+                                             uint32_t& pl, uint32_t& nptr, uint32_t tab,
+                                             uint32_t s_ids,
                                              uint8_t* pay, uint32_t* fl32, uint32_t lane,
                                              unsigned long long* hist) {
     const bool valid = lane < cnt;
@@ -113,7 +127,7 @@ __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32
     const uint32_t vm = cnt >= 32 ? kFull : ((1u << cnt) - 1u);
     const uint32_t lm = lanemask_lt();
     const uint32_t at = pl + 2u * __popc(pm & lm) + uint32_t(S) * __popc(vm & ~pm & lm);
-    const uint32_t id = (valid && !isptr) ? uint32_t(ids[tokv]) : 0u;
+    const uint32_t id = (valid && !isptr) ? lds_u8(s_ids + tokv) : 0u;
     const uint32_t sym = __shfl_sync(kFull, tab, id);
     if (valid) {
         if (isptr) {
@@ -135,6 +149,7 @@ __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32
     }
     if (lane == 0) fl32[t0 >> 5] = __byte_perm(__brev(pm), 0u, 0x0123);
     pl += 2u * __popc(pm) + uint32_t(S) * __popc(vm & ~pm);
+    nptr += __popc(pm);
 }
 
 // Pass 1: rename the chunk's symbols to ids 0..D-1 (first-occurrence order)
@@ -270,50 +285,50 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
         build_rows<NW>(ids, n, D, rows, RW, lane);
 
         // ---- greedy walk (encoder.cpp:25-41); lane t % 32 holds token t
-        // until the batch of 32 is flushed straight into the chunk's slots
+        // until the batch of 32 is flushed straight into the chunk's slots.
+        // Token 0 is the literal at position 0 (empty window).
         uint8_t* pay = a.pay_slots + ck * uint64_t(C) * S;
         uint32_t* fl32 = reinterpret_cast<uint32_t*>(a.flag_slots + ck * uint64_t(C / 8));
-        int p = 0;
-        uint32_t t = 0, pl = 0, tokv = 0, nptr = 0;
+        const uint32_t s_ids = static_cast<uint32_t>(__cvta_generic_to_shared(ids));
+        const uint32_t s_rows = static_cast<uint32_t>(__cvta_generic_to_shared(rows));
+        int p = 1;
+        uint32_t slot = 1, tb = 0, pl = 0, tokv = 0, nptr = 0;
         while (p < n) {
             uint32_t K = 0, off = 0;
-            if (p > 0 && (p & Im1) == 0) {
-                // bit b of word jw <-> candidate w = p - W + 32*jw + b
+            if ((p & Im1) == 0) {
+                // bit b of word jw <-> candidate w = p - W + 32*jw + b.
+                // Step k + grp reads the id of position p + k + grp (clamped
+                // to n: the zero row) and the row bits from p + qc + k; the
+                // next round's ids are loaded a round ahead.
                 uint32_t A = shl_clamp(kFull, uint32_t(max(lbc - p, 0)));
                 uint32_t x, nz;
-                // step k + grp reads id x[p + k + grp] (clamped to position
-                // n, the zero row) and the row words at bit p + qc + k; the
-                // next round's loads are issued before this round's shuffles
-                const uint8_t* idp = ids + p + grp;
+                const uint32_t ib = s_ids + uint32_t(p + grp);
                 const int lim = n - p - grp;
-                const uint32_t* rq = rows + ((p + qc) >> 5);
-                int sh = (p + qc) & 31, k = 0;
-                const uint32_t* r = rq + uint32_t(idp[min(0, lim)]) * RW;
-                uint32_t lo = r[0], hi = r[1];
-                uint32_t idn = idp[min(G, lim)];
+                int q = p + qc;               // row bit cursor (advances G per round)
+                const int mk = clg - q;       // mask shift of the round: max(mk + q, 0)
+                const int ik = lim + q;       // id index clamp: min(q - q0, lim) = min(q, ik) - q0
+                const int q0 = q;
+                uint32_t id = lds_u8(ib + uint32_t(min(0, lim)));
+                uint32_t idn = lds_u8(ib + uint32_t(min(G, lim)));
+#pragma unroll 2
                 for (;;) {
-                    const int shn = sh + G;
-                    const uint32_t* rqn = rq + (shn >> 5);
-                    const uint32_t* rn = rqn + idn * RW;
-                    const uint32_t lon = rn[0], hin = rn[1];
-                    idn = idp[min(k + 2 * G, lim)];
-                    const uint32_t f = __funnelshift_r(lo, hi, uint32_t(sh));
-                    x = f & shr_clamp(kFull, uint32_t(max(clg + k, 0))) & A;
+                    const uint32_t ra = s_rows + id * uint32_t(RW * 4) + uint32_t((q >> 5) << 2);
+                    const uint32_t lo = lds_u32(ra), hi = lds_u32(ra + 4);
+                    id = idn;
+                    idn = lds_u8(ib + uint32_t(min(q + 2 * G, ik) - q0));
+                    const uint32_t f = __funnelshift_r(lo, hi, uint32_t(q));
+                    x = f & shr_clamp(kFull, uint32_t(max(mk + q, 0))) & A;
 #pragma unroll
                     for (int d = 1; d < G; d <<= 1) x &= __shfl_up_sync(kFull, x, d * NW);
                     nz = __ballot_sync(kFull, x != 0u);
                     const uint32_t An = __shfl_sync(kFull, x, (G - 1) * NW + jw);
                     if ((nz >> (32 - NW)) == 0u) break;  // the search ends in this round
                     A = An;
-                    k += G;
-                    sh = shn & 31;
-                    rq = rqn;
-                    lo = lon;
-                    hi = hin;
+                    q += G;
                 }
                 // steps matched in the last round: groups with non-empty sets
                 const int e = (static_cast<int>(31 - __clz(nz)) + NW) >> LNW;  // nz == 0 -> 0
-                K = uint32_t(k + e);
+                K = uint32_t(q - q0 + e);
                 if (K >= min_match) {
                     // winner: lowest set bit of A_K (group e-1 of x, or A)
                     const uint32_t val = e > 0 ? x : A;
@@ -324,14 +339,16 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
                 }
             }
             const bool ptr = K >= min_match;
-            if (lane == (t & 31u)) tokv = ptr ? (0x80000000u | K | (off << 8)) : uint32_t(p);
+            if (lane == slot) tokv = ptr ? (0x80000000u | K | (off << 8)) : uint32_t(p);
             p += ptr ? static_cast<int>(K) : 1;
-            nptr += ptr ? 1u : 0u;
-            ++t;
-            if ((t & 31u) == 0)
-                flush_tokens<S>(tokv, 32u, t - 32u, pl, tab, ids, pay, fl32, lane, a.hist);
+            if (++slot == 32u) {
+                flush_tokens<S>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
+                slot = 0;
+                tb += 32u;
+            }
         }
-        if (t & 31u) flush_tokens<S>(tokv, t & 31u, t & ~31u, pl, tab, ids, pay, fl32, lane, a.hist);
+        if (slot) flush_tokens<S>(tokv, slot, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
+        const uint32_t t = tb + slot;
         if (lane == 0) {
             a.psize[ck] = pl;
             a.fsize[ck] = (t + 7u) >> 3;
