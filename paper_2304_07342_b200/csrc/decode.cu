@@ -227,10 +227,11 @@ __device__ __forceinline__ bool header_params_ok(uint32_t S, uint32_t W, uint32_
     return true;  // C % I == 0 and the default block_bytes follow from the sets
 }
 
-__global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
+__global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
     __shared__ uint64_t s_at, s_out, s_chunks, s_j, s_n, s_maxcb;
     __shared__ unsigned long long s_bad;
-    __shared__ uint32_t s_stop;
+    __shared__ uint32_t s_stop, s_err;
+    __shared__ uint64_t s_eoff;
     const uint32_t tid = threadIdx.x;
     ParseResult* res = a.result;
     if (tid == 0) {
@@ -298,20 +299,6 @@ __global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
         }
         __syncthreads();
         if (s_stop) break;
-        {
-            // ---- table monotonicity, first violation in (entry, payload-first) order
-            const uint8_t* ptab = a.img + s_at + 26;
-            const uint64_t n = s_n;
-            const uint8_t* ftab = ptab + 4 * (n + 1);
-            for (uint64_t i = tid; i < n; i += blockDim.x) {
-                if (ld_le32(ptab + 4 * (i + 1)) < ld_le32(ptab + 4 * i)) {
-                    atomicMin(&s_bad, 2 * i);
-                } else if (ld_le32(ftab + 4 * (i + 1)) < ld_le32(ftab + 4 * i)) {
-                    atomicMin(&s_bad, 2 * i + 1);
-                }
-            }
-        }
-        __syncthreads();
         if (tid == 0) {
             const uint64_t at = s_at, n = s_n;
             const uint8_t* b = a.img + at;
@@ -324,11 +311,7 @@ __global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
             const uint64_t orig = ld_le64(b + 13);
             const uint64_t ftot = ld_le32(ftab + 4 * n), ptot = ld_le32(ptab + 4 * n);
             const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + tail;
-            if (s_bad != ~0ull) {
-                const uint64_t i = s_bad >> 1;
-                err = (s_bad & 1) ? PE_FLAG_MONO : PE_PAYLOAD_MONO;
-                eoff = (s_bad & 1) ? 26 + 4 * (n + 1) + 4 * (i + 1) : 26 + 4 * (i + 1);
-            } else if (ld_le32(ptab) != 0) {
+            if (ld_le32(ptab) != 0) {
                 err = PE_PAYLOAD_START;
                 eoff = 26;
             } else if (ld_le32(ftab) != 0) {
@@ -349,6 +332,42 @@ __global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
             } else if (s_out + orig > a.out_cap) {
                 err = PE_CAPACITY;
             }
+            s_err = err;
+            s_eoff = eoff;
+        }
+        __syncthreads();
+        if (s_err != PE_OK) {
+            // the reference checks table monotonicity before these (format.cpp
+            // order); a container that passes them has its monotonicity
+            // checked by the decode kernel from the entries each chunk reads
+            const uint8_t* ptab = a.img + s_at + 26;
+            const uint64_t n = s_n;
+            const uint8_t* ftab = ptab + 4 * (n + 1);
+            for (uint64_t i = tid; i < n; i += blockDim.x) {
+                if (ld_le32(ptab + 4 * (i + 1)) < ld_le32(ptab + 4 * i)) {
+                    atomicMin(&s_bad, 2 * i);
+                } else if (ld_le32(ftab + 4 * (i + 1)) < ld_le32(ftab + 4 * i)) {
+                    atomicMin(&s_bad, 2 * i + 1);
+                }
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const uint64_t at = s_at, n = s_n;
+            const uint8_t* b = a.img + at;
+            const uint64_t S = b[5], C = ld_le32(b + 9), tail = b[25];
+            const uint64_t orig = ld_le64(b + 13);
+            const uint8_t* ptab = b + 26;
+            const uint8_t* ftab = ptab + 4 * (n + 1);
+            const uint64_t ftot = ld_le32(ftab + 4 * n), ptot = ld_le32(ptab + 4 * n);
+            const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + tail;
+            uint32_t err = s_err;
+            uint64_t eoff = s_eoff;
+            if (s_bad != ~0ull) {
+                const uint64_t i = s_bad >> 1;
+                err = (s_bad & 1) ? PE_FLAG_MONO : PE_PAYLOAD_MONO;
+                eoff = (s_bad & 1) ? 26 + 4 * (n + 1) + 4 * (i + 1) : 26 + 4 * (i + 1);
+            }
             if (err != PE_OK) {
                 res->err_kind = err;
                 res->err_container = s_j;
@@ -362,6 +381,7 @@ __global__ void __launch_bounds__(1024) plz_parse_kernel(DecodeArgs a) {
                 d.chunk_base = s_chunks;
                 d.flags_off = at + 26 + 8 * (n + 1);
                 d.payload_off = d.flags_off + ftot;
+                d.payload_len = ptot;
                 d.original_len = orig;
                 d.num_chunks = uint32_t(n);
                 d.chunk_size = uint32_t(C);
@@ -410,6 +430,20 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     v |= __shfl_xor_sync(0xffffffffu, v, 2);
     const uint32_t p0 = __shfl_sync(0xffffffffu, v, 0), p1 = __shfl_sync(0xffffffffu, v, 4);
     const uint32_t f0 = __shfl_sync(0xffffffffu, v, 8), f1 = __shfl_sync(0xffffffffu, v, 12);
+    // table monotonicity (format.cpp order: payload entry before flag entry);
+    // a violating chunk is not decoded — the whole container is corrupt
+    if (p1 < p0 || f1 < f0) {
+        if (lane == 0 && a.mono_key)
+            atomicMin(a.mono_key, (unsigned long long)((d.chunk_base + k) << 1) | (p1 < p0 ? 0ull : 1ull));
+        *err_tok = 0;
+        return TE_OK;
+    }
+    // an entry past its stream's end implies a decrease further on (the last
+    // entry is the stream size): skip, the violating chunk reports it
+    if (p1 > d.payload_len || f1 > d.payload_off - d.flags_off) {
+        *err_tok = 0;
+        return TE_OK;
+    }
     const uint64_t C = d.chunk_size;
     const uint64_t L = (k + 1 == d.num_chunks) ? d.last_len : C;
     uint8_t* dst = a.out + d.out_off + k * C * S;
@@ -498,6 +532,21 @@ __global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* 
     }
 }
 
+// The first monotonicity violation the decode kernel found: the container,
+// its first chunk (errors of lower chunks belong to earlier containers and
+// win), and the reference's byte offset of the offending entry.
+__global__ void plz_mono_detail_kernel(DecodeArgs a, unsigned long long key, uint64_t* base) {
+    const uint64_t g = key >> 1;
+    const uint64_t j = find_container(a.desc, a.result->n_containers, g);
+    const ContainerDesc d = a.desc[j];
+    const uint64_t i = g - d.chunk_base, n = d.num_chunks;
+    ParseResult* r = a.result;
+    r->err_kind = (key & 1) ? PE_FLAG_MONO : PE_PAYLOAD_MONO;
+    r->err_container = j;
+    r->err_offset = (key & 1) ? 26 + 4 * (n + 1) + 4 * (i + 1) : 26 + 4 * (i + 1);
+    *base = d.chunk_base;
+}
+
 __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
     __shared__ uint32_t tab[33];
     const uint32_t lane = lane_id();
@@ -535,7 +584,7 @@ int decode_ctas_per_sm() {
 }
 
 void launch_parse(const DecodeArgs& a, cudaStream_t st) {
-    plz_parse_kernel<<<1, 1024, 0, st>>>(a);
+    plz_parse_kernel<<<1, 256, 0, st>>>(a);
 }
 
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
@@ -547,6 +596,11 @@ void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st) {
     plz_chunk_detail_kernel<<<1, 32, kDecodeWarpSmem, st>>>(a, code, chunk, token);
+}
+
+void launch_mono_detail(const DecodeArgs& a, unsigned long long key, uint64_t* base,
+                        cudaStream_t st) {
+    plz_mono_detail_kernel<<<1, 1, 0, st>>>(a, key, base);
 }
 
 void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {

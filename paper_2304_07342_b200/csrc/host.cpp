@@ -174,6 +174,8 @@ struct Meta {
     uint64_t detail_chunk;
     uint64_t detail_token;
     unsigned long long err_chunk;
+    unsigned long long mono_key;  // first table-monotonicity violation, ~0 if none
+    uint64_t mono_base;           // first chunk of its container
     uint32_t work[8];  // [0] encode, [1] scan tiles, [2] assemble/decode, [4] fallback
                        // count, [5] wide-pass counter
     uint32_t stalled;  // H2D pipeline: a segment never arrived
@@ -468,7 +470,7 @@ int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_
     Meta* m = dmeta(c);
     if (c->desc.cap < 64 * sizeof(ContainerDesc)) CK(c->desc.ensure(64 * sizeof(ContainerDesc)));
     CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
-    CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk, st));
+    CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk + sizeof m->mono_key, st));
     CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
     DecodeArgs a{};
     a.img = d_img;
@@ -480,6 +482,7 @@ int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_
     a.result = &m->parse;
     a.out_len = d_out_len;
     a.err_chunk = &m->err_chunk;
+    a.mono_key = &m->mono_key;
     a.work = &m->work[2];
     launch_parse(a, st);
     int per_sm = decode_ctas_per_sm();
@@ -500,6 +503,16 @@ int finish_decompress(plzgpu_ctx* c, cudaStream_t st, bool* grow, plzgpu_error* 
     CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     *grow = false;
+    if (h.mono_key != ~0ull) {
+        // a table-monotonicity violation in container j: chunk errors of
+        // earlier containers come first (decoder order), then this one
+        Meta* m = dmeta(c);
+        launch_mono_detail(c->last_decode, h.mono_key, &m->mono_base, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h.err_chunk == ~0ull || h.err_chunk >= h.mono_base) return parse_error(h.parse, err);
+    }
     if (h.err_chunk != ~0ull) {
         Meta* m = dmeta(c);
         launch_chunk_detail(c->last_decode, &m->detail_code, &m->detail_chunk, &m->detail_token, st);
@@ -877,7 +890,7 @@ int plzgpu_decompress_async(plzgpu_ctx* c, const void* d_img, uint64_t len, void
         CK(cudaMemsetAsync(d_out_len, 0, 8, st));
         Meta* m = dmeta(c);
         CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
-        CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk, st));
+        CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk + sizeof m->mono_key, st));
         c->last_launches = 0;
         c->last_op = OP_NONE;
         return PLZGPU_OK;

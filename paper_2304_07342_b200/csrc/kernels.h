@@ -188,6 +188,7 @@ struct ContainerDesc {
     uint64_t chunk_base;         // global index of the container's chunk 0
     uint64_t flags_off;          // absolute image offset of the flag stream
     uint64_t payload_off;        // absolute image offset of the payload stream
+    uint64_t payload_len;        // payload stream bytes (the last payload-table entry)
     uint64_t original_len;
     uint32_t num_chunks;
     uint32_t chunk_size;
@@ -222,6 +223,9 @@ struct DecodeArgs {
     uint64_t* out_len;           // device word (async API)
     unsigned long long* err_chunk;  // min failing global chunk (atomicMin), ~0 if none
     uint32_t* work;
+    // first table-monotonicity violation (global chunk << 1 | flag table),
+    // ~0 if none; null: not checked (size-only walks)
+    unsigned long long* mono_key;
 };
 void launch_parse(const DecodeArgs& a, cudaStream_t st);
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
@@ -242,5 +246,8 @@ struct DecodeOneArgs {
     uint64_t* err_token;
 };
 void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st);
+// ParseResult error fields for a monotonicity key; *base = the container's first chunk
+void launch_mono_detail(const DecodeArgs& a, unsigned long long key, uint64_t* base,
+                        cudaStream_t st);
 
 }  // namespace plzgpu

@@ -103,16 +103,17 @@ def test_configs_bit_exact(S, W, C, I, kind):
 
 @pytest.mark.parametrize("S,C", [(2, 2048), (2, 1024), (4, 1024), (4, 4096)])
 def test_symbol_dictionary_boundary(S, C):
-    # Kernel I renames a chunk's symbols to 8-bit ids; chunks with more than
-    # 256 distinct symbols go to the wide-cell pass.  Chunks with 1, 7, 255,
-    # 256, 257 and C distinct symbols (extremes of the value range included),
-    # interleaved, must all give the reference image.
+    # Kernel I's bitmap pass keeps one occurrence row per distinct symbol of a
+    # chunk (at most kBmMaxSyms = 16); chunks with more go to the wide-cell
+    # pass.  Chunks with 1, 3, 7, 15, 16, 17, 255, 256, 257 and C distinct
+    # symbols (extremes of the value range included), interleaved, must all
+    # give the reference image.
     import numpy as np
 
     rng = np.random.default_rng(S * 100000 + C)
     top = (1 << (8 * S)) - 1
     chunks = []
-    for d in (7, 256, 257, 1, 255, C, 256, 3):
+    for d in (7, 16, 17, 256, 257, 1, 15, 255, C, 16, 3):
         if d == 1:
             alphabet = np.array([top], dtype=np.uint64)
         else:
@@ -206,6 +207,49 @@ def test_corrupted_images_raise_the_reference_error():
             assert plz.decompress_bytes(bad) == ref_decompress(bad)
         same += 1
     assert same == 300
+
+
+def _table_entry(img, j_container, table, i, value):
+    """Overwrite entry i of container j's payload (table 0) or flag (table 1)
+    offset table in a concatenated image."""
+    import struct
+
+    at = 0
+    for _ in range(j_container):
+        n = struct.unpack_from("<I", img, at + 21)[0]
+        ptot = struct.unpack_from("<I", img, at + 26 + 4 * n)[0]
+        ftot = struct.unpack_from("<I", img, at + 26 + 4 * (n + 1) + 4 * n)[0]
+        at += 26 + 8 * (n + 1) + ftot + ptot + img[at + 25]
+    n = struct.unpack_from("<I", img, at + 21)[0]
+    struct.pack_into("<I", img, at + 26 + table * 4 * (n + 1) + 4 * i, value)
+
+
+def test_table_monotonicity_errors_in_reference_order():
+    # The decode kernel checks each chunk's own table entries (format.cpp
+    # checks the whole table before decoding any chunk): the reported error
+    # must still be the reference's — chunk errors of earlier containers
+    # first, then the first decreasing entry (payload before flag) — and
+    # entries pointing past their stream must not be read.
+    data = inputs.make("runs", 60000, 11, 2)
+    p = P(2, 128, 1024, 1, 1024 * 2 * 8)  # 8 chunks per container, 4 containers
+    img = plz.compress(data, p)
+    cases = []
+    for j, table, i, val in [(0, 0, 3, 0), (1, 1, 5, 0), (2, 0, 1, 0xFFFFFF00),
+                             (3, 1, 2, 0xFFFFFFFF), (1, 0, 7, 1), (0, 1, 1, 0x7FFFFFFF)]:
+        bad = bytearray(img)
+        _table_entry(bad, j, table, i, val)
+        cases.append(bytes(bad))
+    # a payload byte flip in container 0's chunk 1 together with a decreasing
+    # entry in container 2: the chunk error comes first
+    bad = bytearray(cases[2])
+    n0 = int.from_bytes(bad[21:25], "little")
+    f0 = int.from_bytes(bad[26 + 4 * (n0 + 1) + 4 * n0: 26 + 4 * (n0 + 1) + 4 * n0 + 4], "little")
+    flags_at = 26 + 8 * (n0 + 1)
+    for k in range(40):
+        bad[flags_at + f0 + k] ^= 0x5A
+    cases.append(bytes(bad))
+    for bad in cases:
+        assert _err(plz.decompress_bytes, bad) == _err(ref_decompress, bad)
 
 
 def test_truncations_raise_the_reference_error():
