@@ -196,6 +196,144 @@ __device__ uint32_t decode_chunk_warp(const uint8_t* __restrict__ flags, uint64_
     return TE_OK;
 }
 
+// Shared-memory symbol access by 32-bit shared-window address.
+template <int S>
+__device__ __forceinline__ uint32_t lds_sym(uint32_t a) {
+    uint32_t v;
+    if constexpr (S == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    else if constexpr (S == 2) asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
+    else asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+template <int S>
+__device__ __forceinline__ void sts_sym(uint32_t a, uint32_t v) {
+    if constexpr (S == 1) asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v));
+    else if constexpr (S == 2) asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "r"(v));
+    else asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// decode_chunk_warp for the common case — the chunk's output fits the warp's
+// shared-memory stage — with chunk-local 32-bit positions and shared-window
+// addresses.  Same token semantics and error order.  A pointer position q
+// copies from q - off (the forward byte copy of decoder.cpp:80-84: for a
+// malformed len > off the source lies inside the same token and the chase
+// below follows it back), chasing sources that fall in the same 32-position
+// wave back to a literal or an earlier wave.
+template <int S>
+__device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_t nf,
+                                      const uint8_t* __restrict__ pay, uint32_t np, uint32_t L,
+                                      uint32_t s_out, uint32_t s_tab, uint32_t lane,
+                                      uint64_t* err_tok) {
+    uint32_t written = 0, in = 0, t = 0;
+    const uint32_t below = (1u << lane) - 1u, upto = (2u << lane) - 1u;
+    while (written < L) {
+        const uint32_t tt = t + lane;
+        const bool hf = (tt >> 3) < nf;
+        const uint32_t bit = hf ? (uint32_t(flags[tt >> 3]) >> (7u - (tt & 7u))) & 1u : 0u;
+        const uint32_t pmask = __ballot_sync(0xffffffffu, bit);
+        const uint32_t nptr = __popc(pmask & below);
+        const uint32_t pin = in + 2u * nptr + uint32_t(S) * (lane - nptr);
+        const uint32_t sz = bit ? 2u : uint32_t(S);
+        const bool has = pin + sz <= np;
+        uint32_t len = 0, off = 0, lit = 0;
+        if (has) {
+            if (bit) {
+                len = pay[pin];
+                off = pay[pin + 1];
+            } else {
+#pragma unroll
+                for (int b = 0; b < S; ++b) lit |= uint32_t(pay[pin + b]) << (8 * b);
+            }
+        }
+        const uint32_t adv = bit ? len : 1u;
+        const uint32_t incl = warp_incl_scan_u32(adv, lane);
+        const uint32_t rel = incl - adv;  // < 32*255
+        const uint32_t pos = written + rel;
+        const bool reached = pos < L;
+        uint32_t e = TE_OK;
+        if (!hf) e = TE_FLAGS_EXHAUSTED;
+        else if (!has) e = TE_PAYLOAD_EXHAUSTED;
+        else if (bit) {
+            if (len == 0 || off == 0) e = TE_ZERO_FIELD;
+            else if (off > pos) e = TE_OFFSET_BEFORE_START;
+            else if (pos + len > L) e = TE_OVERRUN;
+        }
+        const uint32_t m_end = __ballot_sync(0xffffffffu, !reached);
+        const uint32_t m_err = __ballot_sync(0xffffffffu, e != TE_OK && reached);
+        const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
+        const uint32_t first_err = m_err ? uint32_t(__ffs(m_err) - 1) : 32u;
+        if (first_err < first_end) {
+            *err_tok = uint64_t(t) + first_err;
+            return __shfl_sync(0xffffffffu, e, first_err);
+        }
+        const bool act = lane < first_end;
+        if (act && !bit) sts_sym<S>(s_out + pos * S, lit);
+        const uint32_t la = first_end - 1;
+        const uint32_t span = __shfl_sync(0xffffffffu, incl, la);
+        if (pmask & (first_end >= 32u ? 0xffffffffu : (1u << first_end) - 1u)) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_tab + 4u * lane),
+                         "r"((rel << 16) | (bit << 8) | off));
+            __syncwarp();
+            uint32_t before = 0;  // batch tokens starting before the wave
+            for (uint32_t wbase = 0; wbase < span; wbase += 32) {
+                const uint32_t d = rel - wbase;
+                const uint32_t starts =
+                    __reduce_or_sync(0xffffffffu, (act && d < 32u) ? 1u << d : 0u);
+                const uint32_t q = wbase + lane;
+                if (q < span) {
+                    const uint32_t ent = lds32(s_tab + 4u * (before + __popc(starts & upto) - 1u));
+                    if (ent & 0x100u) {
+                        // batch-relative source; negative = an earlier batch (final)
+                        int src = int(q) - int(ent & 0xffu);
+                        while (src >= int(wbase)) {  // source in this wave: chase it back
+                            const uint32_t i = uint32_t(src) - wbase;
+                            const uint32_t e2 = lds32(
+                                s_tab + 4u * (before + __popc(starts & ((2u << i) - 1u)) - 1u));
+                            if (!(e2 & 0x100u)) break;  // a literal: already written
+                            src -= int(e2 & 0xffu);
+                        }
+                        sts_sym<S>(s_out + (written + q) * S,
+                                   lds_sym<S>(s_out + uint32_t(int(written) + src) * S));
+                    }
+                }
+                before += __popc(starts);
+                __syncwarp();
+            }
+        }
+        written += span;
+        in = __shfl_sync(0xffffffffu, pin + sz, la);
+        t += first_end;
+    }
+    if (in != np) {
+        *err_tok = t;
+        return TE_TRAILING_PAYLOAD;
+    }
+    // padding bits after the last token must be zero (decoder.cpp:61-63)
+    const uint32_t b0 = t >> 3;
+    for (uint32_t base = b0; base < nf; base += 32) {
+        const uint32_t bi = base + lane;
+        uint32_t v = bi < nf ? flags[bi] : 0u;
+        if (bi == b0) v &= 0xffu >> (t & 7u);
+        const uint32_t m = __ballot_sync(0xffffffffu, v != 0u);
+        if (m) {
+            const int l = __ffs(m) - 1;
+            const uint32_t vv = __shfl_sync(0xffffffffu, v, l);
+            *err_tok = 8 * (uint64_t(base) + uint64_t(l)) + uint64_t(__clz(vv) - 24);
+            return TE_NONZERO_PADDING;
+        }
+    }
+    if (nf != ((t + 7) >> 3)) {
+        *err_tok = t;
+        return TE_FLAG_COUNT;
+    }
+    return TE_OK;
+}
+
 // ------------------------------------------------------------------ parse
 enum ParseErr : uint32_t {
     PE_OK = 0,
@@ -454,8 +592,9 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem);
     if (in_smem)
-        e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{stage}, tab,
-                                        lane, &tok);
+        e = decode_chunk_smem<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L),
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(stage)),
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(tab)), lane, &tok);
     else if ((reinterpret_cast<uintptr_t>(dst) & (S - 1)) == 0)
         e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, tab,
                                         lane, &tok);
