@@ -28,7 +28,10 @@ namespace {
 constexpr int kDecodeWarps = 8;
 constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 KiB chunks;
                                         // larger chunks decode in global memory)
-constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144;  // + token table (16-B aligned)
+// + token table (128 B, 16-B aligned) + start bitmap of a batch's span
+// (one bit per output position: kDecodeSmem / 32 words cover any chunk that
+// decodes in shared memory)
+constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144 + kDecodeSmem / 8;
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -219,18 +222,22 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 
 // decode_chunk_warp for the common case — the chunk's output fits the warp's
 // shared-memory stage — with chunk-local 32-bit positions and shared-window
-// addresses.  Same token semantics and error order.  A pointer position q
+// addresses.  Same token semantics and error order.  Per batch of 32 tokens:
+// literals are stored straight away; token starts are OR-ed into a bitmap of
+// the batch's span (one bit per output position), so in each 32-position wave
+// a lane finds its covering token with one popcount.  A pointer position q
 // copies from q - off (the forward byte copy of decoder.cpp:80-84: for a
 // malformed len > off the source lies inside the same token and the chase
-// below follows it back), chasing sources that fall in the same 32-position
-// wave back to a literal or an earlier wave.
+// follows it back), chasing sources in the same wave back to a literal or an
+// earlier wave.
 template <int S>
 __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_t nf,
                                       const uint8_t* __restrict__ pay, uint32_t np, uint32_t L,
-                                      uint32_t s_out, uint32_t s_tab, uint32_t lane,
-                                      uint64_t* err_tok) {
+                                      uint32_t s_out, uint32_t s_tab, uint32_t* bm,
+                                      uint32_t lane, uint64_t* err_tok) {
     uint32_t written = 0, in = 0, t = 0;
     const uint32_t below = (1u << lane) - 1u, upto = (2u << lane) - 1u;
+    const uint32_t s_bm = static_cast<uint32_t>(__cvta_generic_to_shared(bm));
     while (written < L) {
         const uint32_t tt = t + lane;
         const bool hf = (tt >> 3) < nf;
@@ -255,19 +262,21 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
         const uint32_t rel = incl - adv;  // < 32*255
         const uint32_t pos = written + rel;
         const bool reached = pos < L;
-        uint32_t e = TE_OK;
-        if (!hf) e = TE_FLAGS_EXHAUSTED;
-        else if (!has) e = TE_PAYLOAD_EXHAUSTED;
-        else if (bit) {
-            if (len == 0 || off == 0) e = TE_ZERO_FIELD;
-            else if (off > pos) e = TE_OFFSET_BEFORE_START;
-            else if (pos + len > L) e = TE_OVERRUN;
-        }
+        const bool bad = !has || (bit && (len == 0 || off == 0 || off > pos || pos + len > L));
         const uint32_t m_end = __ballot_sync(0xffffffffu, !reached);
-        const uint32_t m_err = __ballot_sync(0xffffffffu, e != TE_OK && reached);
         const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
-        const uint32_t first_err = m_err ? uint32_t(__ffs(m_err) - 1) : 32u;
-        if (first_err < first_end) {
+        const uint32_t m_err = __ballot_sync(0xffffffffu, bad && reached);
+        if (m_err && uint32_t(__ffs(m_err) - 1) < first_end) {
+            // the first failing token, classified in decoder.cpp:22-66 order
+            uint32_t e = TE_OK;
+            if (!hf) e = TE_FLAGS_EXHAUSTED;
+            else if (!has) e = TE_PAYLOAD_EXHAUSTED;
+            else if (bit) {
+                if (len == 0 || off == 0) e = TE_ZERO_FIELD;
+                else if (off > pos) e = TE_OFFSET_BEFORE_START;
+                else if (pos + len > L) e = TE_OVERRUN;
+            }
+            const uint32_t first_err = uint32_t(__ffs(m_err) - 1);
             *err_tok = uint64_t(t) + first_err;
             return __shfl_sync(0xffffffffu, e, first_err);
         }
@@ -277,30 +286,44 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
         const uint32_t span = __shfl_sync(0xffffffffu, incl, la);
         if (pmask & (first_end >= 32u ? 0xffffffffu : (1u << first_end) - 1u)) {
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_tab + 4u * lane),
-                         "r"((rel << 16) | (bit << 8) | off));
+                         "r"((bit << 8) | off));
+            const uint32_t nw = (span + 31u) >> 5;
+#pragma unroll 1
+            for (uint32_t w = lane; w < nw; w += 32) bm[w] = 0u;
             __syncwarp();
+            if (act) atomicOr(&bm[rel >> 5], 1u << (rel & 31u));
+            __syncwarp();
+            // Branch-free waves: every lane copies out[q] = out[src]; literal
+            // positions and positions past the span copy onto themselves.
+            const uint32_t s_w = s_out + written * S;
             uint32_t before = 0;  // batch tokens starting before the wave
-            for (uint32_t wbase = 0; wbase < span; wbase += 32) {
-                const uint32_t d = rel - wbase;
-                const uint32_t starts =
-                    __reduce_or_sync(0xffffffffu, (act && d < 32u) ? 1u << d : 0u);
-                const uint32_t q = wbase + lane;
-                if (q < span) {
-                    const uint32_t ent = lds32(s_tab + 4u * (before + __popc(starts & upto) - 1u));
-                    if (ent & 0x100u) {
-                        // batch-relative source; negative = an earlier batch (final)
-                        int src = int(q) - int(ent & 0xffu);
-                        while (src >= int(wbase)) {  // source in this wave: chase it back
-                            const uint32_t i = uint32_t(src) - wbase;
-                            const uint32_t e2 = lds32(
-                                s_tab + 4u * (before + __popc(starts & ((2u << i) - 1u)) - 1u));
-                            if (!(e2 & 0x100u)) break;  // a literal: already written
-                            src -= int(e2 & 0xffu);
+#pragma unroll 1
+            for (uint32_t w = 0; w < nw; ++w) {
+                const uint32_t starts = lds32(s_bm + 4u * w);
+                const uint32_t q = (w << 5) + lane;
+                const uint32_t ent = lds32(s_tab + 4u * (before + __popc(starts & upto) - 1u));
+                const bool cp = q < span && (ent & 0x100u);
+                // batch-relative source; negative = an earlier batch (final)
+                int src = cp ? int(q) - int(ent & 0xffu) : int(q);
+                if (__any_sync(0xffffffffu, cp && src >= int(w << 5))) {
+                    // some source lies in this wave: chase it back to a
+                    // literal or an earlier wave
+                    bool more = cp;
+                    while (__any_sync(0xffffffffu, more)) {
+                        if (more) {
+                            if (src < int(w << 5)) {
+                                more = false;
+                            } else {
+                                const uint32_t i = uint32_t(src) & 31u;
+                                const uint32_t e2 = lds32(
+                                    s_tab + 4u * (before + __popc(starts & ((2u << i) - 1u)) - 1u));
+                                if (e2 & 0x100u) src -= int(e2 & 0xffu);
+                                else more = false;
+                            }
                         }
-                        sts_sym<S>(s_out + (written + q) * S,
-                                   lds_sym<S>(s_out + uint32_t(int(written) + src) * S));
                     }
                 }
+                sts_sym<S>(s_w + q * S, lds_sym<S>(uint32_t(int(s_w) + src * S)));
                 before += __popc(starts);
                 __syncwarp();
             }
@@ -594,7 +617,9 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     if (in_smem)
         e = decode_chunk_smem<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L),
                                  static_cast<uint32_t>(__cvta_generic_to_shared(stage)),
-                                 static_cast<uint32_t>(__cvta_generic_to_shared(tab)), lane, &tok);
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(tab)),
+                                 reinterpret_cast<uint32_t*>(stage + kDecodeSmem + 144), lane,
+                                 &tok);
     else if ((reinterpret_cast<uintptr_t>(dst) & (S - 1)) == 0)
         e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, tab,
                                         lane, &tok);
