@@ -28,10 +28,12 @@ namespace {
 constexpr int kDecodeWarps = 8;
 constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 KiB chunks;
                                         // larger chunks decode in global memory)
-// + token table (128 B, 16-B aligned) + start bitmap of a batch's span
-// (one bit per output position: kDecodeSmem / 32 words cover any chunk that
-// decodes in shared memory)
-constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + 144 + kDecodeSmem / 8;
+// + pad (a wave writes up to 31 positions past its batch's span) + token
+// table (128 B) + start bitmap of a batch's span (one bit per output
+// position: kDecodeSmem / 32 words cover any chunk that decodes in shared
+// memory)
+constexpr uint32_t kDecodePad = 128;
+constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSmem / 8;
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -285,45 +287,44 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
         const uint32_t la = first_end - 1;
         const uint32_t span = __shfl_sync(0xffffffffu, incl, la);
         if (pmask & (first_end >= 32u ? 0xffffffffu : (1u << first_end) - 1u)) {
+            // token table: -off for a pointer, 0 for a literal (its positions
+            // then copy onto themselves)
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_tab + 4u * lane),
-                         "r"((bit << 8) | off));
+                         "r"(bit ? 0u - off : 0u));
             const uint32_t nw = (span + 31u) >> 5;
 #pragma unroll 1
             for (uint32_t w = lane; w < nw; w += 32) bm[w] = 0u;
             __syncwarp();
             if (act) atomicOr(&bm[rel >> 5], 1u << (rel & 31u));
             __syncwarp();
-            // Branch-free waves: every lane copies out[q] = out[src]; literal
-            // positions and positions past the span copy onto themselves.
+            // Waves: every lane copies out[q] = out[src].  Positions past the
+            // span (at most 31) land in the stage's pad or in positions a
+            // later batch rewrites.
             const uint32_t s_w = s_out + written * S;
+            const uint32_t s_tb = s_tab - 4u;  // index before + popc - 1
             uint32_t before = 0;  // batch tokens starting before the wave
 #pragma unroll 1
             for (uint32_t w = 0; w < nw; ++w) {
                 const uint32_t starts = lds32(s_bm + 4u * w);
-                const uint32_t q = (w << 5) + lane;
-                const uint32_t ent = lds32(s_tab + 4u * (before + __popc(starts & upto) - 1u));
-                const bool cp = q < span && (ent & 0x100u);
+                const int q = int(w << 5) + int(lane);
+                const int tv = int(lds32(s_tb + 4u * (before + __popc(starts & upto))));
                 // batch-relative source; negative = an earlier batch (final)
-                int src = cp ? int(q) - int(ent & 0xffu) : int(q);
-                if (__any_sync(0xffffffffu, cp && src >= int(w << 5))) {
-                    // some source lies in this wave: chase it back to a
-                    // literal or an earlier wave
-                    bool more = cp;
-                    while (__any_sync(0xffffffffu, more)) {
+                int src = q + tv;
+                bool more = tv != 0 && src >= int(w << 5) && q < int(span);
+                if (__any_sync(0xffffffffu, more)) {
+                    // a source in this wave: chase it back to a literal or an
+                    // earlier wave
+                    do {
                         if (more) {
-                            if (src < int(w << 5)) {
-                                more = false;
-                            } else {
-                                const uint32_t i = uint32_t(src) & 31u;
-                                const uint32_t e2 = lds32(
-                                    s_tab + 4u * (before + __popc(starts & ((2u << i) - 1u)) - 1u));
-                                if (e2 & 0x100u) src -= int(e2 & 0xffu);
-                                else more = false;
-                            }
+                            const uint32_t i = uint32_t(src) & 31u;
+                            const int t2 = int(lds32(
+                                s_tb + 4u * (before + __popc(starts & ((2u << i) - 1u)))));
+                            src += t2;
+                            more = t2 != 0 && src >= int(w << 5);
                         }
-                    }
+                    } while (__any_sync(0xffffffffu, more));
                 }
-                sts_sym<S>(s_w + q * S, lds_sym<S>(uint32_t(int(s_w) + src * S)));
+                sts_sym<S>(s_w + uint32_t(q) * S, lds_sym<S>(uint32_t(int(s_w) + src * S)));
                 before += __popc(starts);
                 __syncwarp();
             }
@@ -613,12 +614,13 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     const uint8_t* py = a.img + d.payload_off + p0;
     uint64_t tok = 0;
     uint32_t e;
-    uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem);
+    uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
     if (in_smem)
         e = decode_chunk_smem<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L),
                                  static_cast<uint32_t>(__cvta_generic_to_shared(stage)),
                                  static_cast<uint32_t>(__cvta_generic_to_shared(tab)),
-                                 reinterpret_cast<uint32_t*>(stage + kDecodeSmem + 144), lane,
+                                 reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad + 144),
+                                 lane,
                                  &tok);
     else if ((reinterpret_cast<uintptr_t>(dst) & (S - 1)) == 0)
         e = decode_chunk_warp<S, false>(fl, f1 - f0, py, p1 - p0, L, SymOut<S, false>{dst}, tab,
