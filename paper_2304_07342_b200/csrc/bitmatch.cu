@@ -29,9 +29,10 @@
 //
 // Occurrence bitmaps need one row per distinct symbol of the chunk (quant
 // codes: 3-9 per 2048-symbol chunk).  The chunk's symbols are renamed to
-// ids 0..D-1 (first occurrence order); a chunk with more than kBmMaxSyms
-// distinct symbols is listed for the wide-cell pass (encode.cu), which
-// handles any alphabet.
+// ids 0..D-1 (first occurrence order).  The first pass keeps 16 rows per
+// warp (28 warps/SM at c2); a chunk with more distinct symbols is listed for
+// a second bitmap pass with 64 rows, and one with more than 64 for the
+// wide-cell pass (encode.cu), which handles any alphabet.
 #include "common.cuh"
 
 namespace plzgpu {
@@ -115,9 +116,9 @@ __device__ __forceinline__ bool stage_chunk(const EncodeArgs& a, uint64_t ck, in
 // symbols come from the id table (lane d of `tab` holds id d's symbol).  The
 // flag word is the ballot of pointer lanes, bit-reversed within each byte
 // (MSB-first, encoder.cpp:33).
-template <int S>
+template <int S, int NT>
 __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32_t t0,
-                                             uint32_t& pl, uint32_t& nptr, uint32_t tab,
+                                             uint32_t& pl, uint32_t& nptr, const uint32_t (&tab)[NT],
                                              uint32_t s_ids,
                                              uint8_t* pay, uint32_t* fl32, uint32_t lane,
                                              unsigned long long* hist) {
@@ -128,7 +129,12 @@ __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32
     const uint32_t lm = lanemask_lt();
     const uint32_t at = pl + 2u * __popc(pm & lm) + uint32_t(S) * __popc(vm & ~pm & lm);
     const uint32_t id = (valid && !isptr) ? lds_u8(s_ids + tokv) : 0u;
-    const uint32_t sym = __shfl_sync(kFull, tab, id);
+    uint32_t sym = __shfl_sync(kFull, tab[0], id & 31u);
+#pragma unroll
+    for (int r = 1; r < NT; ++r) {
+        const uint32_t v = __shfl_sync(kFull, tab[r], id & 31u);
+        sym = (id >> 5) == uint32_t(r) ? v : sym;
+    }
     if (valid) {
         if (isptr) {
             if constexpr (S == 1) {
@@ -154,25 +160,30 @@ __device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32
 
 // Pass 1: rename the chunk's symbols to ids 0..D-1 (first-occurrence order)
 // in place (id i lands on byte i <= S*i, after word i/32 is read), through a
-// small open-addressing table; lane d of the warp keeps id d's symbol in tab.
-// New symbols (at most kBmMaxSyms per chunk, so rare) are inserted one
-// distinct value at a time.  Returns false when the chunk has more than
-// kBmMaxSyms distinct symbols.
-template <int S>
+// small open-addressing table; lane d % 32 of the warp keeps id d's symbol in
+// tab[d / 32].  New symbols (at most MAXS per chunk, so rare) are inserted
+// one distinct value at a time.  Returns false when the chunk has more than
+// MAXS distinct symbols.
+template <int S, int MAXS>
 __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, uint32_t lane,
-                                               int& D, uint32_t& tab) {
+                                               int& D, uint32_t (&tab)[(MAXS + 31) / 32]) {
     using T = typename Sym<S>::T;
     constexpr uint32_t kEmpty = 0xffffffffu;
-    tbl[lane] = make_uint2(0u, kEmpty);  // kBmHash == 32 entries
+    constexpr int H = 2 * MAXS;  // table slots: load factor <= 1/2
+    constexpr int HB = MAXS == 16 ? 5 : 7;
+    static_assert((1 << HB) == H, "hash size");
+#pragma unroll
+    for (int i = 0; i < H / 32; ++i) tbl[i * 32 + lane] = make_uint2(0u, kEmpty);
     __syncwarp();
     const T* rs = reinterpret_cast<const T*>(raw);
     D = 0;
-    tab = 0;
+#pragma unroll
+    for (int r = 0; r < (MAXS + 31) / 32; ++r) tab[r] = 0;
     for (int wi = 0; wi * 32 < n; ++wi) {
         const int i = wi * 32 + static_cast<int>(lane);
         const bool valid = i < n;
         const uint32_t v = valid ? uint32_t(rs[i]) : 0u;
-        uint32_t h = (v * 0x9E3779B1u) >> 27, id = kEmpty;
+        uint32_t h = (v * 0x9E3779B1u) >> (32 - HB), id = kEmpty;
         if (valid) {
             for (;;) {
                 const uint2 e = tbl[h];
@@ -181,7 +192,7 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
                     id = e.y;
                     break;
                 }
-                h = (h + 1u) & (kBmHash - 1);
+                h = (h + 1u) & (H - 1);
             }
         }
         const bool missing = valid && id == kEmpty;
@@ -192,13 +203,15 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
                 const int l = __ffs(lead) - 1;
                 lead &= lead - 1;
                 const uint32_t vl = __shfl_sync(kFull, v, l);
-                if (D == kBmMaxSyms) return false;
+                if (D == MAXS) return false;
                 if (lane == 0) {
-                    uint32_t hh = (vl * 0x9E3779B1u) >> 27;
-                    while (tbl[hh].y != kEmpty) hh = (hh + 1u) & (kBmHash - 1);
+                    uint32_t hh = (vl * 0x9E3779B1u) >> (32 - HB);
+                    while (tbl[hh].y != kEmpty) hh = (hh + 1u) & (H - 1);
                     tbl[hh] = make_uint2(vl, uint32_t(D));
                 }
-                if (static_cast<int>(lane) == D) tab = vl;
+#pragma unroll
+                for (int r = 0; r < (MAXS + 31) / 32; ++r)
+                    if (static_cast<int>(lane) + 32 * r == D) tab[r] = vl;
                 if (missing && v == vl) id = uint32_t(D);
                 ++D;
                 __syncwarp();
@@ -230,7 +243,7 @@ __device__ __forceinline__ void build_rows(uint8_t* ids, int n, int D, uint32_t*
     __syncwarp();
 }
 
-template <int S, int NW>
+template <int S, int NW, int MAXS>
 __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs a) {
     constexpr int G = 32 / NW;
     constexpr int LNW = NW == 1 ? 0 : NW == 2 ? 1 : NW == 4 ? 2 : 3;
@@ -241,10 +254,10 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     const int C = a.C, W = a.W;
     const int RW = bm_row_words(C, W);
     // [mbarrier 16][hash table][region: raw chunk -> ids [0, C) + rows at C]
-    uint8_t* base = smem + bm_warp_smem(C, S, W) * warp;
+    uint8_t* base = smem + bm_warp_smem(C, S, W, MAXS) * warp;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base);
     uint2* tbl = reinterpret_cast<uint2*>(base + 16);
-    uint8_t* raw = base + 16 + kBmHash * 8;
+    uint8_t* raw = base + 16 + 2 * MAXS * 8;
     uint8_t* ids = raw;
     uint32_t* rows = reinterpret_cast<uint32_t*>(raw + C);
 
@@ -263,7 +276,11 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
 
     for (;;) {
         uint64_t ck = 0;
-        if (lane == 0) ck = atomicAdd(a.work, 1u);
+        if (lane == 0) {
+            const uint32_t idx = atomicAdd(a.work, 1u);
+            if (!a.src_list) ck = idx;
+            else ck = idx < *a.src_count ? a.src_list[idx] : a.n_chunks;
+        }
         ck = __shfl_sync(kFull, ck, 0);
         if (ck >= a.n_chunks) break;
         const int n = (ck + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : C;
@@ -275,8 +292,8 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
         }
 
         int D;
-        uint32_t tab;
-        if (!rename_symbols<S>(raw, n, tbl, lane, D, tab)) {
+        uint32_t tab[(MAXS + 31) / 32];
+        if (!rename_symbols<S, MAXS>(raw, n, tbl, lane, D, tab)) {
             // too many distinct symbols: the wide-cell pass takes this chunk
             if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1u)] = uint32_t(ck);
             __syncwarp();
@@ -342,12 +359,12 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
             if (lane == slot) tokv = ptr ? (0x80000000u | K | (off << 8)) : uint32_t(p);
             p += ptr ? static_cast<int>(K) : 1;
             if (++slot == 32u) {
-                flush_tokens<S>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
+                flush_tokens<S, (MAXS + 31) / 32>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
                 slot = 0;
                 tb += 32u;
             }
         }
-        if (slot) flush_tokens<S>(tokv, slot, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
+        if (slot) flush_tokens<S, (MAXS + 31) / 32>(tokv, slot, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
         const uint32_t t = tb + slot;
         if (lane == 0) {
             a.psize[ck] = pl;
@@ -363,29 +380,35 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     }
 }
 
-template <int S>
+template <int S, int MAXS>
 const void* bitmatch_fn_s(int nw) {
     switch (nw) {
-        case 1: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 1>);
-        case 2: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 2>);
-        case 4: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 4>);
-        default: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 8>);
+        case 1: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 1, MAXS>);
+        case 2: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 2, MAXS>);
+        case 4: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 4, MAXS>);
+        default: return reinterpret_cast<const void*>(plz_bitmatch_kernel<S, 8, MAXS>);
     }
 }
 
-const void* bitmatch_fn(int S, int W) {
+template <int MAXS>
+const void* bitmatch_fn_m(int S, int nw) {
+    if (S == 1) return bitmatch_fn_s<1, MAXS>(nw);
+    if (S == 2) return bitmatch_fn_s<2, MAXS>(nw);
+    return bitmatch_fn_s<4, MAXS>(nw);
+}
+
+const void* bitmatch_fn(int S, int W, int maxsyms) {
     const int nw = bm_nw(W);
-    if (S == 1) return bitmatch_fn_s<1>(nw);
-    if (S == 2) return bitmatch_fn_s<2>(nw);
-    return bitmatch_fn_s<4>(nw);
+    return maxsyms == kBmMaxSyms ? bitmatch_fn_m<kBmMaxSyms>(S, nw)
+                                 : bitmatch_fn_m<kBmMaxSymsWide>(S, nw);
 }
 
 }  // namespace
 
-int bitmatch_ctas_per_sm(int S, int C, int W, int warps_per_cta) {
+int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta) {
     int blocks = 0;
-    const size_t smem = bm_warp_smem(C, S, W) * warps_per_cta;
-    const void* fn = bitmatch_fn(S, W);
+    const size_t smem = bm_warp_smem(C, S, W, maxsyms) * warps_per_cta;
+    const void* fn = bitmatch_fn(S, W, maxsyms);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
         cudaSuccess) {
         cudaGetLastError();
@@ -395,9 +418,9 @@ int bitmatch_ctas_per_sm(int S, int C, int W, int warps_per_cta) {
     return blocks;
 }
 
-void launch_bitmatch(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = bm_warp_smem(a.C, S, a.W) * a.warps_per_cta;
-    const void* fn = bitmatch_fn(S, a.W);
+void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = bm_warp_smem(a.C, S, a.W, maxsyms) * a.warps_per_cta;
+    const void* fn = bitmatch_fn(S, a.W, maxsyms);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     void* args[] = {const_cast<EncodeArgs*>(&a)};
     cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);

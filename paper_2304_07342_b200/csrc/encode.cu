@@ -256,8 +256,8 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
     return __reduce_max_sync(0xffffffffu, best);
 }
 
-// Kernel I, wide-cell pass: chunks the bitmap pass (bitmatch.cu) left
-// because their alphabet exceeds kBmMaxSyms (from_list), or every chunk.
+// Kernel I, wide-cell pass: chunks the bitmap passes (bitmatch.cu) left
+// because their alphabet exceeds kBmMaxSymsWide (src_list), or every chunk.
 // Cells keep (symbol, run) in 2S bytes, so any alphabet works.
 template <int S>
 __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
@@ -291,8 +291,8 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
         uint64_t g = 0;
         if (lane == 0) {
             const uint32_t idx = atomicAdd(a.work, 1u);
-            if (!a.from_list) g = idx;
-            else g = idx < *a.fb_count ? a.fb_list[idx] : a.n_chunks;
+            if (!a.src_list) g = idx;
+            else g = idx < *a.src_count ? a.src_list[idx] : a.n_chunks;
         }
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= a.n_chunks) break;

@@ -176,8 +176,9 @@ struct Meta {
     unsigned long long err_chunk;
     unsigned long long mono_key;  // first table-monotonicity violation, ~0 if none
     uint64_t mono_base;           // first chunk of its container
-    uint32_t work[8];  // [0] encode, [1] scan tiles, [2] assemble/decode, [4] fallback
-                       // count, [5] wide-pass counter
+    uint32_t work[8];  // [0] first bitmap pass, [1] scan tiles, [2] assemble/decode,
+                       // [4]/[6] overflow counts of the bitmap passes, [5] second
+                       // bitmap pass, [7] wide pass
     uint32_t stalled;  // H2D pipeline: a segment never arrived
     uint32_t pad;
     ParseResult parse;
@@ -197,8 +198,8 @@ struct plzgpu_ctx {
     int last_launches = 0;
     LastOp last_op = OP_NONE;
     DecodeArgs last_decode{};
-    int enc_wpc[800] = {};   // launch shape cache per (pass, S, C)
-    int enc_ctas[800] = {};
+    int enc_wpc[1440] = {};  // launch shape cache per (pass, S, C)
+    int enc_ctas[1440] = {};
     DevBuf fb;               // chunks the bitmap pass left to the wide pass
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
@@ -223,20 +224,23 @@ cudaStream_t pick(plzgpu_ctx*, void* s) { return static_cast<cudaStream_t>(s); }
 
 Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
 
-// Launch shape of Kernel I (bitmap or wide pass) for (S, C, W), cached per
-// context: warps per CTA that maximise resident warps per SM (shared-memory
-// limited).
-void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, bool bitmap, int* wpc_out,
+// Launch shape of Kernel I for (pass, S, C, W), cached per context: warps
+// per CTA that maximise resident warps per SM (shared-memory limited).
+// maxsyms: the bitmap pass's row budget (kBmMaxSyms / kBmMaxSymsWide), 0 for
+// the wide-cell pass.  per_sm = 0: the pass does not fit.
+void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int* wpc_out,
                   int* per_sm_out) {
-    const int pass = bitmap ? 1 + __builtin_ctz(unsigned(bm_nw(p.window))) : 0;  // 0..4
+    const int pass = maxsyms == 0 ? 0 : (maxsyms == kBmMaxSyms ? 1 : 5) +
+                                             __builtin_ctz(unsigned(bm_nw(p.window)));  // 0..8
     const int key = pass * 160 + p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
     int& wpc = c->enc_wpc[key];
     int& per_sm = c->enc_ctas[key];
     if (wpc == 0) {
         int best_warps = 0;
-        for (int cand = 1; cand <= (bitmap ? kBmMaxThreads / 32 : 16); ++cand) {
-            const int ctas = bitmap ? bitmatch_ctas_per_sm(p.symbol_width, p.chunk_size, p.window, cand)
-                                    : encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
+        for (int cand = 1; cand <= (maxsyms ? kBmMaxThreads / 32 : 16); ++cand) {
+            const int ctas = maxsyms ? bitmatch_ctas_per_sm(p.symbol_width, p.chunk_size, p.window,
+                                                            maxsyms, cand)
+                                     : encode_ctas_per_sm(p.symbol_width, p.chunk_size, cand);
             if (ctas * cand > best_warps) {
                 best_warps = ctas * cand;
                 wpc = cand;
@@ -301,31 +305,48 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
     e.hist = c->enc_hist;
-    // bitmap pass over every chunk, then the wide pass over the chunks whose
-    // alphabet it could not hold
-    int wpc = 1, per_sm = 1;
-    encode_shape(c, p, true, &wpc, &per_sm);
-    const bool bitmap = per_sm > 0;
-    if (bitmap) {
-        CK(c->fb.ensure(G * 4 + 16));
-        e.fb_list = c->fb.as<uint32_t>();
-        e.fb_count = &m->work[4];
-        e.warps_per_cta = wpc;
-        launch_bitmatch(p.symbol_width, e, int(std::min<uint64_t>(uint64_t(c->sms) * per_sm,
-                                                                (G + wpc - 1) / wpc)),
-                        st);
+    // bitmap pass (16 rows) over every chunk, a bitmap pass with 64 rows over
+    // the chunks whose alphabet overflowed it, the wide-cell pass over the rest
+    CK(c->fb.ensure(2 * G * 4 + 16));
+    uint32_t* lists[2] = {c->fb.as<uint32_t>(), c->fb.as<uint32_t>() + G};
+    uint32_t* counts[2] = {&m->work[4], &m->work[6]};
+    const uint32_t* src = nullptr;
+    const uint32_t* src_n = nullptr;
+    uint32_t* works[3] = {&m->work[0], &m->work[5], &m->work[7]};
+    int pass = 0;
+    for (int maxsyms : {kBmMaxSyms, kBmMaxSymsWide}) {
+        int wpc = 1, per_sm = 0;
+        encode_shape(c, p, maxsyms, &wpc, &per_sm);
+        if (per_sm == 0) continue;
+        EncodeArgs b = e;
+        b.work = works[pass];
+        b.src_list = src;
+        b.src_count = src_n;
+        b.fb_list = lists[pass];
+        b.fb_count = counts[pass];
+        if (src) b.ready = nullptr;  // every segment has landed after the first pass
+        b.warps_per_cta = wpc;
+        const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (G + wpc - 1) / wpc);
+        launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), st);
+        ++*launches;
+        src = lists[pass];
+        src_n = counts[pass];
+        ++pass;
+    }
+    {
+        int wpc = 1, per_sm = 1;
+        encode_shape(c, p, 0, &wpc, &per_sm);
+        EncodeArgs f = e;
+        f.work = works[2];
+        f.src_list = src;
+        f.src_count = src_n;
+        if (src) f.ready = nullptr;
+        f.warps_per_cta = wpc;
+        launch_encode(p.symbol_width, f,
+                      int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1), (G + wpc - 1) / wpc)),
+                      st);
         ++*launches;
     }
-    EncodeArgs f = e;
-    f.from_list = bitmap ? 1 : 0;
-    f.work = &m->work[5];
-    if (bitmap) f.ready = nullptr;  // every segment has landed once the bitmap pass ends
-    encode_shape(c, p, false, &wpc, &per_sm);
-    f.warps_per_cta = wpc;
-    launch_encode(p.symbol_width, f, int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1),
-                                                          (G + wpc - 1) / wpc)),
-                  st);
-    ++*launches;
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
     ScanArgs sa{};
@@ -1245,7 +1266,7 @@ int plzgpu_match_table(plzgpu_ctx* c, const plzgpu_params* params, const void* i
     e.I = p.interval;
     e.min_match = std::max(1, p.min_match);
     int wpc = 1, per_sm = 1;
-    encode_shape(c, p, false, &wpc, &per_sm);
+    encode_shape(c, p, 0, &wpc, &per_sm);
     e.warps_per_cta = wpc;
     uint64_t grid = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (g.n_chunks + wpc - 1) / wpc);
     launch_match_table(p.symbol_width, e, int(grid), dl, dof,

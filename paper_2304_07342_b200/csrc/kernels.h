@@ -45,9 +45,9 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
     return (b + 15) & ~size_t(15);
 }
 
-// Bitmap pass of Kernel I (bitmatch.cu): chunks with at most kBmMaxSyms
-// distinct symbols.  Per warp:
-//   [mbarrier 16][id hash table: kBmHash x {key, id} u32 pairs]
+// Bitmap passes of Kernel I (bitmatch.cu): chunks with at most kBmMaxSyms
+// (then kBmMaxSymsWide) distinct symbols.  Per warp:
+//   [mbarrier 16][id hash table: 2*maxsyms x {key, id} u32 pairs]
 //   [region: max(C*S, C + rows) + 16 bytes]
 // The region first holds the raw chunk (TMA target); pass 1 renames the
 // symbols to ids in place (bytes [0, C)); pass 2 builds the occurrence rows
@@ -56,18 +56,18 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 // reaching before position 0) and NW + 3 behind (the search's one-round
 // look-ahead); row D (one past the chunk's last id) is all zero and is the
 // id of position n.
-constexpr int kBmMaxSyms = 16;
-constexpr int kBmHash = 32;          // open addressing, load factor <= 1/2
+constexpr int kBmMaxSyms = 16;      // first bitmap pass: all chunks
+constexpr int kBmMaxSymsWide = 64;  // second bitmap pass: the first pass's overflow
 constexpr int kBmMaxThreads = 128;   // CTA size bound (registers: up to 255 per thread)
 __host__ __device__ inline int bm_nw(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8; }
 __host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 3; }
-__host__ __device__ inline size_t bm_region(int C, int S, int W) {
+__host__ __device__ inline size_t bm_region(int C, int S, int W, int maxsyms) {
     const size_t raw = size_t(C) * S;
-    const size_t rows = size_t(C) + size_t(kBmMaxSyms + 1) * bm_row_words(C, W) * 4;
+    const size_t rows = size_t(C) + size_t(maxsyms + 1) * bm_row_words(C, W) * 4;
     return (raw > rows ? raw : rows) + 16;
 }
-__host__ __device__ inline size_t bm_warp_smem(int C, int S, int W) {
-    const size_t b = 16 + size_t(kBmHash) * 8 + bm_region(C, S, W);
+__host__ __device__ inline size_t bm_warp_smem(int C, int S, int W, int maxsyms) {
+    const size_t b = 16 + size_t(2 * maxsyms) * 8 + bm_region(C, S, W, maxsyms);
     return (b + 15) & ~size_t(15);
 }
 
@@ -91,17 +91,20 @@ struct EncodeArgs {
     uint32_t seg_chunks;
     uint32_t* stalled;           // set if a segment never arrives (bounded wait)
     unsigned long long* hist;    // optional: selected pointer lengths [256]
-    // bitmap pass: chunks with > kBmMaxSyms distinct symbols are appended to
-    // fb_list; the wide pass then takes its chunks from fb_list[0..*fb_count)
+    // chunk source: src_list[0..*src_count) when src_list is set (the passes
+    // after the first), else chunks 0..n_chunks-1
+    const uint32_t* src_list;
+    const uint32_t* src_count;
+    // bitmap passes: chunks whose alphabet does not fit are appended here
     uint32_t* fb_list;
     uint32_t* fb_count;
-    int from_list;               // wide pass: iterate fb_list instead of 0..n_chunks
 };
-// the wide-cell kernel (any alphabet); from_list selects the fallback mode
+// the wide-cell kernel (any alphabet)
 void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
-// the bitmap kernel (bitmatch.cu): chunks with <= kBmMaxSyms distinct symbols
-void launch_bitmatch(int S, const EncodeArgs& a, int grid, cudaStream_t st);
-int bitmatch_ctas_per_sm(int S, int C, int W, int warps_per_cta);
+// the bitmap kernel (bitmatch.cu): chunks with <= maxsyms distinct symbols
+// (maxsyms = kBmMaxSyms or kBmMaxSymsWide)
+void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st);
+int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
 void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
                         unsigned long long* raw_hist, cudaStream_t st);
