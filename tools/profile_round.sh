@@ -9,7 +9,7 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ -c 400 --csv \
     --log-file gpurun_out/launches_$R.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 for k in plz_bitmatch plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $([ $k = plz_bitmatch ] && echo 2 || echo 1) -c 1 \
       -o gpurun_out/prof_${k}_$R python tools/probe.py c2 1 > /dev/null 2>&1
 done
 ls -la gpurun_out
