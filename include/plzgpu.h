@@ -235,6 +235,32 @@ int plzgpu_pointer_histogram(plzgpu_ctx* ctx, const plzgpu_params* params, const
 int plzgpu_profile_encode(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
                           uint64_t n, void* stream, plzgpu_error* err);
 
+/* ---------------------------------- cuSZ dual quantization (use case) */
+
+/* The producer of the quantization codes GPULZ compresses in the paper's
+ * improved cuSZ (PAPER.md "Use-case of gpuLZ", Table 3; no counterpart in
+ * the reference library).  Device buffers only; enqueued on `stream`.
+ *   q    = rint(f * s), s = float32(1 / (2 eb))        (round half to even)
+ *   d    = Lorenzo residual Δx Δy Δz q, q = 0 outside  (x fastest; ny/nz = 1
+ *          give 2-D / 1-D)
+ *   code = d + radius if |d| < radius, else 0          (u16; radius <= 32768)
+ * Outliers (code 0) are listed as (index, d) in index order; *n_outliers (a
+ * host word) receives their count — the call synchronises on `stream` for
+ * it.  More than outlier_cap outliers -> PLZGPU_CAPACITY (the list is
+ * truncated; *n_outliers still holds the full count). */
+int plzgpu_lorenzo_quantize(plzgpu_ctx* ctx, const float* d_field, uint64_t nx, uint64_t ny,
+                            uint64_t nz, double eb, int32_t radius, uint16_t* d_codes,
+                            uint64_t* d_outlier_idx, int32_t* d_outlier_val, uint64_t outlier_cap,
+                            uint64_t* n_outliers, void* stream, plzgpu_error* err);
+
+/* Inverse: codes + outliers -> f' = float32(Σx Σy Σz d) * float32(2 eb),
+ * |f - f'| <= eb up to float32 rounding.  Enqueued on `stream`. */
+int plzgpu_lorenzo_reconstruct(plzgpu_ctx* ctx, const uint16_t* d_codes,
+                               const uint64_t* d_outlier_idx, const int32_t* d_outlier_val,
+                               uint64_t n_outliers, uint64_t nx, uint64_t ny, uint64_t nz,
+                               double eb, int32_t radius, float* d_field, void* stream,
+                               plzgpu_error* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,10 @@ SIGNATURES = [  # every entry point of include/plzgpu.h
                                         C.POINTER(_U64), C.POINTER(_U64), _VP, _E]),
     ("plzgpu_shard_headers", C.c_int, [_VP, _P, _U64, C.POINTER(_U64), _VP, _VP, _U64,
                                        C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_lorenzo_quantize", C.c_int, [_VP, _VP, _U64, _U64, _U64, C.c_double, C.c_int32, _VP,
+                                          _VP, _VP, _U64, C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_lorenzo_reconstruct", C.c_int, [_VP, _VP, _VP, _VP, _U64, _U64, _U64, _U64,
+                                             C.c_double, C.c_int32, _VP, _VP, _E]),
 ]
 
 _lib = None

@@ -253,4 +253,20 @@ void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st);
 void launch_mono_detail(const DecodeArgs& a, unsigned long long key, uint64_t* base,
                         cudaStream_t st);
 
+// ------------------------------------------------ cuSZ dual quantization
+uint64_t lorenzo_tiles(uint64_t n);
+// codes + per-tile outlier counts + their exclusive scan (tile_off[tiles] = total)
+void launch_lorenzo_quantize(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,
+                             int32_t radius, uint16_t* codes, uint32_t* tile_count,
+                             uint64_t* tile_off, cudaStream_t st);
+void launch_outlier_write(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,
+                          const uint16_t* codes, const uint32_t* tile_count,
+                          const uint64_t* tile_off, uint64_t* out_idx, int32_t* out_val,
+                          uint64_t cap, cudaStream_t st);
+// d: n int32 scratch
+void launch_lorenzo_reconstruct(const uint16_t* codes, const uint64_t* out_idx,
+                                const int32_t* out_val, uint64_t n_out, uint64_t nx, uint64_t ny,
+                                uint64_t nz, int32_t radius, float two_eb, int32_t* d, float* f,
+                                int sms, cudaStream_t st);
+
 }  // namespace plzgpu
