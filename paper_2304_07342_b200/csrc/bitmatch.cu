@@ -303,16 +303,33 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
 
         // ---- greedy walk (encoder.cpp:25-41); lane t % 32 holds token t
         // until the batch of 32 is flushed straight into the chunk's slots.
-        // Token 0 is the literal at position 0 (empty window).
+        // Runs of literals the walk cannot avoid — position 0 (empty window)
+        // and the unaligned positions up to the next multiple of I (forced
+        // literals, matcher.cpp:121-123) — are recorded up to 32 at a time.
         uint8_t* pay = a.pay_slots + ck * uint64_t(C) * S;
         uint32_t* fl32 = reinterpret_cast<uint32_t*>(a.flag_slots + ck * uint64_t(C / 8));
         const uint32_t s_ids = static_cast<uint32_t>(__cvta_generic_to_shared(ids));
         const uint32_t s_rows = static_cast<uint32_t>(__cvta_generic_to_shared(rows));
-        int p = 1;
-        uint32_t slot = 1, tb = 0, pl = 0, tokv = 0, nptr = 0;
-        while (p < n) {
+        uint32_t slot = 0, tb = 0, pl = 0, tokv = 0, nptr = 0;
+        auto literals = [&](int from, int to) {  // positions [from, to) as literal tokens
+            while (from < to) {
+                const uint32_t m = min(uint32_t(to - from), 32u - slot);
+                if (lane >= slot && lane < slot + m) tokv = uint32_t(from) + (lane - slot);
+                slot += m;
+                from += int(m);
+                if (slot == 32u) {
+                    flush_tokens<S, (MAXS + 31) / 32>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay,
+                                                      fl32, lane, a.hist);
+                    slot = 0;
+                    tb += 32u;
+                }
+            }
+        };
+        int p = min(Im1 + 1, n);
+        literals(0, p);
+        while (p < n) {  // p is a multiple of I here
             uint32_t K = 0, off = 0;
-            if ((p & Im1) == 0) {
+            {
                 // bit b of word jw <-> candidate w = p - W + 32*jw + b.
                 // Step k + grp reads the id of position p + k + grp (clamped
                 // to n: the zero row) and the row bits from p + qc + k; the
@@ -362,6 +379,11 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
                 flush_tokens<S, (MAXS + 31) / 32>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
                 slot = 0;
                 tb += 32u;
+            }
+            if (p & Im1) {  // forced literals up to the next aligned position
+                const int q = min((p + Im1) & ~Im1, n);
+                literals(p, q);
+                p = q;
             }
         }
         if (slot) flush_tokens<S, (MAXS + 31) / 32>(tokv, slot, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
