@@ -441,7 +441,13 @@ def run_b200(args):
                              "utilisation below is its binding roofline (ncu, profiles/)",
                      "alu_pipe": ({"frac": prof["alu_pipe_pct"] / 100, "issue_active":
                                    prof["issue_active_pct"] / 100, "source": prof["source"]}
-                                  if prof and prof.get("alu_pipe_pct") else None)},
+                                  if prof and prof.get("alu_pipe_pct") else None),
+                     # SURVEY.md §8d's matching unit: one symbol compare per
+                     # (aligned position, window candidate) — the reference
+                     # matcher's work, which Kernel I's bitmaps replace with
+                     # W/32 word operations per step
+                     "match_pairs": {"pairs_per_launch": match_pairs(n, w),
+                                     "pairs_per_s": match_pairs(n, w) / (enc_ms * 1e-3)}},
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
         "gpu_launches": (launches if world == 1 else 4) * args.steps,
         "clocks": clk.summary(),
@@ -465,6 +471,19 @@ def run_b200(args):
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def match_pairs(n_bytes: int, w) -> int:
+    """Σ over chunks Σ over positions p ≡ 0 (mod I) of min(W, p): the
+    candidate pairs the reference's find_match examines."""
+    def per_chunk(m):
+        k = (m + w.I - 1) // w.I                  # aligned positions 0, I, ..., < m
+        full = min(k, w.W // w.I + 1)             # p = j*I <= W: min(W, p) = p
+        s = w.I * full * (full - 1) // 2
+        return s + (k - full) * w.W
+    nsym = n_bytes // w.S
+    chunks, last = divmod(nsym, w.C)
+    return chunks * per_chunk(w.C) + (per_chunk(last) if last else 0)
 
 
 def ncu_profile_facts(kernel: str):
