@@ -13,6 +13,8 @@
 // realigned 128-bit stores; the header kernel (one thread per container)
 // writes the 26-byte header, the final table entries, the tail and the image
 // length, and flags 4-byte table overflow (scan.cpp:43-44).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace plzgpu {
@@ -40,8 +42,10 @@ __global__ void __launch_bounds__(256) plz_assemble_kernel(AssembleArgs a) {
     const uint32_t lane = lane_id();
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
-    for (uint64_t g = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
-         g < a.n_chunks; g += warps) {
+    const uint64_t g_lo = a.j_lo * a.cpb;
+    const uint64_t g_hi = a.j_hi ? min(a.n_chunks, a.j_hi * a.cpb) : a.n_chunks;
+    for (uint64_t g = g_lo + uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         g < g_hi; g += warps) {
         const Geo c = locate(a, g);
         const uint64_t img0 = container_start(a, c.j, c.g0);
         const uint64_t pb = a.P64[c.g0], fb = a.F64[c.g0];
@@ -61,8 +65,8 @@ __global__ void __launch_bounds__(256) plz_assemble_kernel(AssembleArgs a) {
 }
 
 __global__ void plz_headers_kernel(AssembleArgs a) {
-    const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (j >= a.n_blocks) return;
+    const uint64_t j = a.j_lo + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= (a.j_hi ? a.j_hi : a.n_blocks)) return;
     const uint64_t g0 = j * a.cpb;
     const uint64_t n = (j + 1 == a.n_blocks) ? a.n_chunks - g0 : a.cpb;
     const uint64_t pb = a.P64[g0], fb = a.F64[g0];
@@ -159,15 +163,18 @@ void launch_shard_headers(const HeaderDesc* d, uint64_t n_conts, uint8_t* img, i
 
 void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     if (a.n_chunks == 0) return;
-    const uint64_t warps_needed = a.n_chunks;
+    const uint64_t g_lo = a.j_lo * a.cpb;
+    const uint64_t g_hi = a.j_hi ? std::min(a.n_chunks, a.j_hi * a.cpb) : a.n_chunks;
+    const uint64_t warps_needed = g_hi - g_lo;
     uint64_t blocks = (warps_needed + 7) / 8;
     if (blocks > 148ull * 16) blocks = 148ull * 16;
     plz_assemble_kernel<<<unsigned(blocks), 256, 0, st>>>(a);
 }
 
 void launch_headers(const AssembleArgs& a, cudaStream_t st) {
-    if (a.n_blocks == 0) return;
-    plz_headers_kernel<<<unsigned((a.n_blocks + 127) / 128), 128, 0, st>>>(a);
+    const uint64_t nj = (a.j_hi ? a.j_hi : a.n_blocks) - a.j_lo;
+    if (nj == 0) return;
+    plz_headers_kernel<<<unsigned((nj + 127) / 128), 128, 0, st>>>(a);
 }
 
 }  // namespace plzgpu

@@ -15,6 +15,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 #include <string>
 #include <vector>
@@ -129,6 +130,15 @@ StreamWriteValue32Fn stream_write_value32() {
     return fn;
 }
 
+bool is_pinned_host(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 bool is_device_ptr(const void* p) {
     if (!p) return false;
     cudaPointerAttributes a;
@@ -204,6 +214,8 @@ struct plzgpu_ctx {
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t asm_stream = nullptr;  // pipelined compress: per-container Kernel III
+    cudaEvent_t asm_ev[2] = {nullptr, nullptr};
     DevBuf ready;
     uint32_t epoch = 0;
     const uint32_t* pipe_ready = nullptr;  // set while enqueueing a pipelined encode
@@ -224,6 +236,13 @@ namespace {
 cudaStream_t pick(plzgpu_ctx*, void* s) { return static_cast<cudaStream_t>(s); }
 
 Meta* dmeta(plzgpu_ctx* c) { return c->meta.as<Meta>(); }
+
+// A/B switch for measurements (PLZGPU_NO_PIPE_ASM=1: the whole-image path
+// for host compresses); unset in normal use.
+bool getenv_flag(const char* name) {
+    const char* v = std::getenv(name);
+    return v && *v && *v != '0';
+}
 
 // Launch shape of Kernel I for (pass, S, C, W), cached per context: warps
 // per CTA that maximise resident warps per SM (shared-memory limited).
@@ -262,10 +281,14 @@ void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int* wpc_o
 // Kernels I and II over G chunks starting at d_in (chunk g at g*C*S); the
 // last of them has logical length last_len.  Leaves psize/fsize, staging
 // slots and exclusive prefixes P64/F64[0..G] in the context.
+// g0/g1 (a pipelined compress, one container at a time): only chunks
+// [g0, g1) of the G; their prefixes continue from P64/F64[g0].
 int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t G,
                         uint32_t last_len, cudaStream_t st, plzgpu_error* err, int* launches,
-                        bool scan = true) {
+                        bool scan = true, uint64_t g0 = 0, uint64_t g1 = UINT64_MAX) {
     const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
+    if (g1 > G) g1 = G;
+    const uint64_t Gr = g1 - g0;  // chunks of this call
     const uint64_t tiles = (G + kScanTile - 1) / kScanTile;
     CK(c->pay_slots.ensure(G * C * S + 64));
     CK(c->flag_slots.ensure(G * (C / 8) + 64));
@@ -277,31 +300,33 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     CK(c->agg.ensure(tiles * 16 + 16));
     CK(c->incl.ensure(tiles * 16 + 16));
     Meta* m = dmeta(c);
-    CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
+    if (g0 == 0) CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
     CK(cudaMemsetAsync(m->work, 0, sizeof m->work + sizeof m->stalled, st));
     if (G == 0) {
         CK(cudaMemsetAsync(c->p64.p, 0, 8, st));
         CK(cudaMemsetAsync(c->f64.p, 0, 8, st));
         return PLZGPU_OK;
     }
-    CK(cudaMemsetAsync(c->status.p, 0, tiles * 4, st));
+    const uint64_t rtiles = (Gr + kScanTile - 1) / kScanTile;
+    CK(cudaMemsetAsync(c->status.p, 0, rtiles * 4, st));
     // ---- Kernel I
+    const uint8_t* in0 = d_in + g0 * C * S;
     EncodeArgs e{};
-    e.in = d_in;
-    e.pay_slots = c->pay_slots.as<uint8_t>();
-    e.flag_slots = c->flag_slots.as<uint8_t>();
-    e.psize = c->psize.as<uint32_t>();
-    e.fsize = c->fsize.as<uint32_t>();
+    e.in = in0;
+    e.pay_slots = c->pay_slots.as<uint8_t>() + g0 * C * S;
+    e.flag_slots = c->flag_slots.as<uint8_t>() + g0 * (C / 8);
+    e.psize = c->psize.as<uint32_t>() + g0;
+    e.fsize = c->fsize.as<uint32_t>() + g0;
     e.stats = m->stats;
     e.work = &m->work[0];
-    e.n_chunks = G;
-    e.last_len = last_len;
+    e.n_chunks = Gr;
+    e.last_len = g1 == G ? last_len : uint32_t(C);
     e.C = p.chunk_size;
     e.W = p.window;
     e.I = p.interval;
     e.min_match = std::max(1, p.min_match);
-    e.bulk_ok = (reinterpret_cast<uintptr_t>(d_in) & 15u) == 0;
-    e.ready = c->pipe_ready;
+    e.bulk_ok = (reinterpret_cast<uintptr_t>(in0) & 15u) == 0;
+    e.ready = c->pipe_ready ? c->pipe_ready + g0 / c->pipe_seg_chunks : nullptr;
     e.epoch = c->epoch;
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
@@ -327,7 +352,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         b.fb_count = counts[pass];
         if (src) b.ready = nullptr;  // every segment has landed after the first pass
         b.warps_per_cta = wpc;
-        const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (G + wpc - 1) / wpc);
+        const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (Gr + wpc - 1) / wpc);
         launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), st);
         ++*launches;
         src = lists[pass];
@@ -344,7 +369,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         if (src) f.ready = nullptr;
         f.warps_per_cta = wpc;
         launch_encode(p.symbol_width, f,
-                      int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1), (G + wpc - 1) / wpc)),
+                      int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1), (Gr + wpc - 1) / wpc)),
                       st);
         ++*launches;
     }
@@ -353,9 +378,13 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     ScanArgs sa{};
     sa.psize = e.psize;
     sa.fsize = e.fsize;
-    sa.n = G;
-    sa.P64 = c->p64.as<uint64_t>();
-    sa.F64 = c->f64.as<uint64_t>();
+    sa.n = Gr;
+    sa.P64 = c->p64.as<uint64_t>() + g0;
+    sa.F64 = c->f64.as<uint64_t>() + g0;
+    if (g0) {  // continue the earlier containers' totals
+        sa.carry_p = c->p64.as<uint64_t>() + g0;
+        sa.carry_f = c->f64.as<uint64_t>() + g0;
+    }
     sa.status = c->status.as<uint32_t>();
     sa.agg = c->agg.as<ulonglong2>();
     sa.incl = c->incl.as<ulonglong2>();
@@ -409,6 +438,60 @@ int enqueue_compress(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in,
     }
     launch_headers(a, st);
     ++launches;
+    CK(cudaGetLastError());
+    c->last_launches = launches;
+    c->last_op = OP_COMPRESS;
+    return PLZGPU_OK;
+}
+
+// A pipelined compress of a host input (plzgpu_compress): one container at a
+// time on `st` — its Kernel I passes (waiting on the container's H2D
+// segments) and its scan, continuing the earlier containers' prefixes — and
+// its Kernel III + header on c->asm_stream, writing into `img` (the caller's
+// pinned host image, mapped) while `st` goes on with the next container.
+int enqueue_compress_by_container(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in,
+                                  uint64_t n, uint8_t* img, cudaStream_t st, plzgpu_error* err) {
+    const Geometry g = geometry(n, p);
+    if (!c->asm_stream) CK(cudaStreamCreateWithFlags(&c->asm_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t& ev : c->asm_ev)
+        if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    Meta* m = dmeta(c);
+    int launches = 0;
+    for (uint64_t j = 0; j < g.n_blocks; ++j) {
+        const uint64_t g0 = j * g.cpb, g1 = std::min(g.n_chunks, g0 + g.cpb);
+        int rc = enqueue_encode_scan(c, p, d_in, g.n_chunks, g.last_len, st, err, &launches, true,
+                                     g0, g1);
+        if (rc) return rc;
+        CK(cudaEventRecord(c->asm_ev[0], st));
+        CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
+        AssembleArgs a{};
+        a.in = d_in;
+        a.pay_slots = c->pay_slots.as<uint8_t>();
+        a.flag_slots = c->flag_slots.as<uint8_t>();
+        a.psize = c->psize.as<uint32_t>();
+        a.fsize = c->fsize.as<uint32_t>();
+        a.P64 = c->p64.as<uint64_t>();
+        a.F64 = c->f64.as<uint64_t>();
+        a.img = img;
+        a.img_len = &m->img_len;
+        a.overflow = &m->overflow;
+        a.n_bytes = n;
+        a.n_chunks = g.n_chunks;
+        a.cpb = g.cpb;
+        a.block_bytes = p.block_bytes;
+        a.n_blocks = g.n_blocks;
+        a.S = p.symbol_width;
+        a.W = p.window;
+        a.I = p.interval;
+        a.C = p.chunk_size;
+        a.j_lo = j;
+        a.j_hi = j + 1;
+        launch_assemble(a, c->asm_stream);
+        launch_headers(a, c->asm_stream);
+        launches += 2;
+    }
+    CK(cudaEventRecord(c->asm_ev[1], c->asm_stream));
+    CK(cudaStreamWaitEvent(st, c->asm_ev[1], 0));
     CK(cudaGetLastError());
     c->last_launches = launches;
     c->last_op = OP_COMPRESS;
@@ -720,6 +803,12 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
         b->release();
     if (c->host_meta) cudaFreeHost(c->host_meta);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->asm_stream) {
+        cudaStreamSynchronize(c->asm_stream);
+        cudaStreamDestroy(c->asm_stream);
+    }
+    for (cudaEvent_t& ev : c->asm_ev)
+        if (ev) cudaEventDestroy(ev);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
@@ -747,18 +836,29 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
     const uint8_t* d_in = static_cast<const uint8_t*>(in);
     const bool host_in = !is_device_ptr(in);
     const uint64_t bound = plzgpu_compress_bound(n, params);
-    const bool direct = is_device_ptr(out) && cap >= bound;
+    const Geometry geo = geometry(n, *params);
+    const char* seg_env = std::getenv("PLZGPU_SEG_MB");  // A/B: H2D segment size
+    const uint64_t seg_bytes_target = uint64_t(seg_env ? std::max(1, std::atoi(seg_env)) : 32) << 20;
+    const uint64_t chunk_bytes = uint64_t(params->chunk_size) * params->symbol_width;
+    const uint64_t seg_chunks = std::max<uint64_t>(1, seg_bytes_target / chunk_bytes);
+    const uint64_t nseg = (geo.n_chunks + seg_chunks - 1) / seg_chunks;
+    // Host input into a pinned host image of several containers: container
+    // by container, Kernel III writing each one straight into the host
+    // buffer (mapped) while the next container's segments still arrive.
+    void* mapped = nullptr;
+    const bool per_container =
+        host_in && nseg > 1 && geo.n_blocks > 1 && cap >= bound && is_pinned_host(out) &&
+        geo.cpb % 4 == 0 && geo.cpb % seg_chunks == 0 && !getenv_flag("PLZGPU_NO_PIPE_ASM") &&
+        (cudaHostGetDevicePointer(&mapped, out, 0) == cudaSuccess || (cudaGetLastError(), false));
+    const bool direct = (is_device_ptr(out) || per_container) && cap >= bound;
     uint8_t* img = static_cast<uint8_t*>(out);
-    if (!direct) {
+    if (per_container) {
+        img = static_cast<uint8_t*>(mapped);
+    } else if (!direct) {
         CK(c->img.ensure(bound));
         img = c->img.as<uint8_t>();
     }
     Meta* m = dmeta(c);
-    const Geometry geo = geometry(n, *params);
-    const uint64_t seg_bytes_target = uint64_t(32) << 20;
-    const uint64_t chunk_bytes = uint64_t(params->chunk_size) * params->symbol_width;
-    const uint64_t seg_chunks = std::max<uint64_t>(1, seg_bytes_target / chunk_bytes);
-    const uint64_t nseg = (geo.n_chunks + seg_chunks - 1) / seg_chunks;
     StreamWriteValue32Fn write_value = stream_write_value32();
     if (host_in && write_value && nseg > 1) {
         // H2D pipeline: Kernel I starts at once and each warp waits for its
@@ -776,7 +876,11 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
         }
         c->pipe_ready = c->ready.as<uint32_t>();
         c->pipe_seg_chunks = uint32_t(seg_chunks);
-        rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
+        if (per_container) {
+            rc = enqueue_compress_by_container(c, *params, d_in, n, img, st, err);
+        } else {
+            rc = enqueue_compress(c, *params, d_in, n, img, &m->img_len, st, err);
+        }
         c->pipe_ready = nullptr;
         if (rc) return rc;
         for (uint64_t sgi = 0; sgi < nseg; ++sgi) {

@@ -120,6 +120,10 @@ struct ScanArgs {
     ulonglong2* agg;             // per tile (payload, flag) aggregate
     ulonglong2* incl;            // per tile inclusive prefix
     uint32_t* tile_counter;      // zeroed before launch
+    // optional: prefixes start at *carry_p / *carry_f (a container scanned
+    // on its own, continuing the earlier containers' totals)
+    const uint64_t* carry_p;
+    const uint64_t* carry_f;
 };
 void launch_scan(const ScanArgs& a, cudaStream_t st);
 
@@ -142,6 +146,9 @@ struct AssembleArgs {
     uint64_t block_bytes;
     uint64_t n_blocks;
     int S, W, I, C;
+    // containers [j_lo, j_hi) only (their chunks): one container of a
+    // pipelined compress; the defaults (0, 0) mean every container
+    uint64_t j_lo, j_hi;
 };
 void launch_assemble(const AssembleArgs& a, cudaStream_t st);
 void launch_headers(const AssembleArgs& a, cudaStream_t st);

@@ -130,8 +130,13 @@ __global__ void __launch_bounds__(kScanThreads) plz_scan_kernel(ScanArgs a) {
     }
     __syncthreads();
 
-    // ---- write this thread's 8 exclusive prefixes
-    const Pair pre = s_prefix;
+    // ---- write this thread's 8 exclusive prefixes (+ the carry of earlier
+    // containers when the scan covers one container of a pipelined compress)
+    Pair pre = s_prefix;
+    if (a.carry_p) {
+        pre.p += *a.carry_p;
+        pre.f += *a.carry_f;
+    }
     const Pair wex = s_warp[warp];
     unsigned long long rp = pre.p + wex.p + (incl.p - own.p);
     unsigned long long rf = pre.f + wex.f + (incl.f - own.f);

@@ -179,6 +179,28 @@ def test_concatenated_images_with_tails():
     assert ref_decompress(joined) == b"".join(parts)
 
 
+def test_pinned_host_compress_by_container():
+    # A host input of several segments into a pinned host image of several
+    # containers takes the per-container pipeline (Kernel III writing into
+    # the mapped host image); it must give the device path's image, which the
+    # other tests pin to the reference.
+    import numpy as np
+    import torch
+
+    for S, C, bb, size in ((2, 2048, 32 << 20, (100 << 20) + 4097), (4, 1024, 64 << 20, 150 << 20)):
+        p = P(S, 255, C, 2, bb)
+        data = np.frombuffer(inputs.make("quant", size, S + size, S), dtype=np.uint8)
+        h_in = torch.from_numpy(data.copy()).pin_memory()
+        cap = plz.compress_bound(size, p)
+        h_img = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        ctx = plz.context()
+        n_img, _ = ctx.compress_ptr(p, h_in.data_ptr(), size, h_img.data_ptr(), cap)
+        dev = plz.compress(h_in.cuda(), p)
+        assert n_img == dev.numel()
+        assert torch.equal(h_img[:n_img], dev.cpu())
+        assert torch.equal(plz.decompress_bytes(dev), h_in.cuda())
+
+
 def test_device_resident_path_matches_host_path():
     import torch
 
