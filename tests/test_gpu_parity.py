@@ -199,6 +199,10 @@ def test_pinned_host_compress_by_container():
         assert n_img == dev.numel()
         assert torch.equal(h_img[:n_img], dev.cpu())
         assert torch.equal(plz.decompress_bytes(dev), h_in.cuda())
+        # and back into a pinned host output (written by the decode kernel)
+        h_out = torch.empty(size, dtype=torch.uint8).pin_memory()
+        assert ctx.decompress_ptr(h_img.data_ptr(), n_img, h_out.data_ptr(), size) == size
+        assert torch.equal(h_out, h_in)
 
 
 def test_device_resident_path_matches_host_path():
