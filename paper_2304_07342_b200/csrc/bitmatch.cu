@@ -31,8 +31,8 @@
 // codes: 3-9 per 2048-symbol chunk).  The chunk's symbols are renamed to
 // ids 0..D-1 (first occurrence order).  The first pass keeps 16 rows per
 // warp (28 warps/SM at c2); a chunk with more distinct symbols is listed for
-// a second bitmap pass with 64 rows, and one with more than 64 for the
-// wide-cell pass (encode.cu), which handles any alphabet.
+// a second bitmap pass with 32 rows, then a third with 64, and one with more
+// than 64 for the wide-cell pass (encode.cu), which handles any alphabet.
 #include "common.cuh"
 
 namespace plzgpu {
@@ -170,7 +170,7 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
     using T = typename Sym<S>::T;
     constexpr uint32_t kEmpty = 0xffffffffu;
     constexpr int H = 2 * MAXS;  // table slots: load factor <= 1/2
-    constexpr int HB = MAXS == 16 ? 5 : 7;
+    constexpr int HB = MAXS == 16 ? 5 : MAXS == 32 ? 6 : 7;
     static_assert((1 << HB) == H, "hash size");
 #pragma unroll
     for (int i = 0; i < H / 32; ++i) tbl[i * 32 + lane] = make_uint2(0u, kEmpty);
@@ -421,8 +421,9 @@ const void* bitmatch_fn_m(int S, int nw) {
 
 const void* bitmatch_fn(int S, int W, int maxsyms) {
     const int nw = bm_nw(W);
-    return maxsyms == kBmMaxSyms ? bitmatch_fn_m<kBmMaxSyms>(S, nw)
-                                 : bitmatch_fn_m<kBmMaxSymsWide>(S, nw);
+    return maxsyms == kBmMaxSyms      ? bitmatch_fn_m<kBmMaxSyms>(S, nw)
+           : maxsyms == kBmMaxSymsMid ? bitmatch_fn_m<kBmMaxSymsMid>(S, nw)
+                                      : bitmatch_fn_m<kBmMaxSymsWide>(S, nw);
 }
 
 }  // namespace

@@ -186,9 +186,9 @@ struct Meta {
     unsigned long long err_chunk;
     unsigned long long mono_key;  // first table-monotonicity violation, ~0 if none
     uint64_t mono_base;           // first chunk of its container
-    uint32_t work[8];  // [0] first bitmap pass, [1] scan tiles, [2] assemble/decode,
-                       // [4]/[6] overflow counts of the bitmap passes, [5] second
-                       // bitmap pass, [7] wide pass
+    uint32_t work[12];  // [0] first bitmap pass, [1] scan tiles, [2] assemble/decode,
+                        // [4]/[6]/[8] overflow counts of the bitmap passes, [5]/[9]
+                        // second/third bitmap pass, [7] wide pass
     uint32_t stalled;  // H2D pipeline: a segment never arrived
     uint32_t pad;
     ParseResult parse;
@@ -208,8 +208,8 @@ struct plzgpu_ctx {
     int last_launches = 0;
     LastOp last_op = OP_NONE;
     DecodeArgs last_decode{};
-    int enc_wpc[1440] = {};  // launch shape cache per (pass, S, C)
-    int enc_ctas[1440] = {};
+    int enc_wpc[2240] = {};  // launch shape cache per (pass, S, C)
+    int enc_ctas[2240] = {};
     DevBuf fb;               // chunks the bitmap pass left to the wide pass
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
@@ -250,8 +250,8 @@ bool getenv_flag(const char* name) {
 // the wide-cell pass.  per_sm = 0: the pass does not fit.
 void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int* wpc_out,
                   int* per_sm_out) {
-    const int pass = maxsyms == 0 ? 0 : (maxsyms == kBmMaxSyms ? 1 : 5) +
-                                             __builtin_ctz(unsigned(bm_nw(p.window)));  // 0..8
+    const int pass = maxsyms == 0 ? 0 : (maxsyms == kBmMaxSyms ? 1 : maxsyms == kBmMaxSymsMid ? 5 : 9) +
+                                             __builtin_ctz(unsigned(bm_nw(p.window)));  // 0..12
     const int key = pass * 160 + p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
     int& wpc = c->enc_wpc[key];
     int& per_sm = c->enc_ctas[key];
@@ -333,14 +333,15 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.hist = c->enc_hist;
     // bitmap pass (16 rows) over every chunk, a bitmap pass with 64 rows over
     // the chunks whose alphabet overflowed it, the wide-cell pass over the rest
-    CK(c->fb.ensure(2 * G * 4 + 16));
-    uint32_t* lists[2] = {c->fb.as<uint32_t>(), c->fb.as<uint32_t>() + G};
-    uint32_t* counts[2] = {&m->work[4], &m->work[6]};
+    CK(c->fb.ensure(3 * G * 4 + 16));
+    uint32_t* lists[3] = {c->fb.as<uint32_t>(), c->fb.as<uint32_t>() + G,
+                          c->fb.as<uint32_t>() + 2 * G};
+    uint32_t* counts[3] = {&m->work[4], &m->work[6], &m->work[8]};
     const uint32_t* src = nullptr;
     const uint32_t* src_n = nullptr;
-    uint32_t* works[3] = {&m->work[0], &m->work[5], &m->work[7]};
+    uint32_t* works[4] = {&m->work[0], &m->work[5], &m->work[9], &m->work[7]};
     int pass = 0;
-    for (int maxsyms : {kBmMaxSyms, kBmMaxSymsWide}) {
+    for (int maxsyms : {kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide}) {
         int wpc = 1, per_sm = 0;
         encode_shape(c, p, maxsyms, &wpc, &per_sm);
         if (per_sm == 0) continue;
@@ -363,7 +364,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         int wpc = 1, per_sm = 1;
         encode_shape(c, p, 0, &wpc, &per_sm);
         EncodeArgs f = e;
-        f.work = works[2];
+        f.work = works[3];
         f.src_list = src;
         f.src_count = src_n;
         if (src) f.ready = nullptr;

@@ -57,7 +57,8 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 // look-ahead); row D (one past the chunk's last id) is all zero and is the
 // id of position n.
 constexpr int kBmMaxSyms = 16;      // first bitmap pass: all chunks
-constexpr int kBmMaxSymsWide = 64;  // second bitmap pass: the first pass's overflow
+constexpr int kBmMaxSymsMid = 32;   // second bitmap pass: the first pass's overflow
+constexpr int kBmMaxSymsWide = 64;  // third bitmap pass: the second pass's overflow
 constexpr int kBmMaxThreads = 128;   // CTA size bound (registers: up to 255 per thread)
 __host__ __device__ inline int bm_nw(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8; }
 __host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 3; }
@@ -102,7 +103,7 @@ struct EncodeArgs {
 // the wide-cell kernel (any alphabet)
 void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
 // the bitmap kernel (bitmatch.cu): chunks with <= maxsyms distinct symbols
-// (maxsyms = kBmMaxSyms or kBmMaxSymsWide)
+// (maxsyms = kBmMaxSyms, kBmMaxSymsMid or kBmMaxSymsWide)
 void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st);
 int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram

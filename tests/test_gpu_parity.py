@@ -103,17 +103,17 @@ def test_configs_bit_exact(S, W, C, I, kind):
 
 @pytest.mark.parametrize("S,C", [(2, 2048), (2, 1024), (4, 1024), (4, 4096)])
 def test_symbol_dictionary_boundary(S, C):
-    # Kernel I's first bitmap pass keeps one occurrence row per distinct
-    # symbol of a chunk (at most 16), the second at most 64; chunks with more
-    # go to the wide-cell pass.  Chunks with 1, 3, 7, 15, 16, 17, 63, 64, 65,
-    # 255, 256, 257 and C distinct symbols (extremes of the value range
-    # included), interleaved, must all give the reference image.
+    # Kernel I's bitmap passes keep one occurrence row per distinct symbol of
+    # a chunk (at most 16, then 32, then 64); chunks with more go to the
+    # wide-cell pass.  Chunks with 1, 3, 7, 15-17, 31-33, 63-65, 255-257 and
+    # C distinct symbols (extremes of the value range included), interleaved,
+    # must all give the reference image.
     import numpy as np
 
     rng = np.random.default_rng(S * 100000 + C)
     top = (1 << (8 * S)) - 1
     chunks = []
-    for d in (7, 16, 17, 64, 256, 65, 257, 1, 15, 63, 255, C, 16, 3):
+    for d in (7, 16, 17, 32, 64, 256, 33, 65, 257, 1, 15, 31, 63, 255, C, 16, 3):
         if d == 1:
             alphabet = np.array([top], dtype=np.uint64)
         else:
@@ -137,13 +137,13 @@ def test_symbol_dictionary_boundary(S, C):
 
 @pytest.mark.parametrize("C,W", [(4096, 128), (1024, 32), (2048, 255)])
 def test_byte_alphabet_boundaries(C, W):
-    # S = 1: chunks with 1..256 distinct byte values across both bitmap
-    # passes' limits (16, 64) and the wide-cell pass
+    # S = 1: chunks with 1..256 distinct byte values across the bitmap
+    # passes' limits (16, 32, 64) and the wide-cell pass
     import numpy as np
 
     rng = np.random.default_rng(C + W)
     chunks = []
-    for d in (7, 16, 17, 63, 64, 65, 200, 256, 1, 3):
+    for d in (7, 16, 17, 31, 32, 33, 63, 64, 65, 200, 256, 1, 3):
         alphabet = rng.permutation(256)[:d].astype(np.uint8)
         idx = np.concatenate([np.arange(d), rng.integers(0, d, C - d)])
         idx = np.repeat(idx, rng.integers(1, 5, C))[:C]
