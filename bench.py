@@ -402,7 +402,7 @@ def run_b200(args):
 
     total_in = n * world
     peak, peak_kind = load_peaks()
-    prof = ncu_profile_facts("plz_bitmatch_kernel")
+    prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {[1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]}, 16>")
     enc_bytes = n + n_img  # input read + staged tokens written (~ image)
     achieved = enc_bytes / (enc_ms * 1e-3) / 1e9
     line = {

@@ -8,8 +8,12 @@ timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$R.json 2> 
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ -c 400 --csv \
     --log-file gpurun_out/launches_$R.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-for k in plz_bitmatch plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $([ $k = plz_bitmatch ] && echo 2 || echo 1) -c 1 \
+# Kernel I: the first bitmap pass (16 rows) of the second compress call
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+    -k 'regex:plz_bitmatch_kernel<.*16>' -s 1 -c 1 \
+    -o gpurun_out/prof_plz_bitmatch_$R python tools/probe.py c2 1 > /dev/null 2>&1
+for k in plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/prof_${k}_$R python tools/probe.py c2 1 > /dev/null 2>&1
 done
 ls -la gpurun_out
