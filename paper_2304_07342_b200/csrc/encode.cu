@@ -258,7 +258,8 @@ __device__ __forceinline__ uint32_t find_match_warp(const typename Sym<S>::Cell*
 
 // Kernel I, wide-cell pass: chunks the bitmap passes (bitmatch.cu) left
 // because their alphabet exceeds kBmMaxSymsWide (src_list), or every chunk.
-// Cells keep (symbol, run) in 2S bytes, so any alphabet works.
+// Cells keep (symbol, run) in 2S bytes, so any alphabet works; tokens leave
+// in 32-token batches as in the bitmap passes.
 template <int S>
 __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     using T = typename Sym<S>::T;
@@ -270,12 +271,9 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
     const int C = a.C;
     constexpr size_t kHead = size_t(kEncodeHeadPerS) * S;
     uint8_t* base = smem + encode_warp_smem(C, S) * warp;
-    // [payload head: kHead B][cells: C x sizeof(Cell)][flags: C/8 B][list][mbarrier]
-    // Payload byte b is stored at head[b]: beyond kHead it runs on into the
-    // cell array.  It is written at a step p with b < S*(p+1) <= kHead +
-    // sizeof(Cell)*(p-W), i.e. over cells left of the window that are never
-    // read again (see encode_warp_smem).
-    uint8_t* head = base;
+    // [head: kHead B][cells: C x sizeof(Cell)][flags: C/8 B][list][mbarrier]
+    // (the head and flag areas are the layout plz_match_table_kernel shares;
+    // this kernel writes its tokens straight to the slots)
     Cell* cells = reinterpret_cast<Cell*>(base + kHead);
     uint8_t* raw8 = base + kHead + size_t(C) * S;  // raw stage: the upper half of the cells
     uint8_t* flg = base + kHead + size_t(C) * sizeof(Cell);      // C/8 bytes
@@ -364,53 +362,85 @@ __global__ void __launch_bounds__(512) plz_encode_kernel(EncodeArgs a) {
             __syncwarp();
         }
 
-        // ---- greedy walk (encoder.cpp:25-41) with on-demand matching.  Flag
-        // bits gather in a 32-token word: token t is bit (t % 32) ^ 7 of the
-        // little-endian word, i.e. MSB-first within each byte.
+        // ---- greedy walk (encoder.cpp:25-41) with on-demand matching; lane
+        // t % 32 holds token t until the batch of 32 is flushed straight into
+        // the chunk's slots (literal symbols read back from the cells).
+        // Position 0 and the unaligned positions up to the next multiple of
+        // I are literals recorded up to 32 at a time.
         const int I = a.I, W = a.W, min_match = a.min_match;
-        int p = 0;
-        uint32_t t = 0, pl = 0, fw = 0, nptr = 0;
-        while (p < n) {
-            uint32_t key = 0;
-            if (p > 0 && (p & (I - 1)) == 0) key = find_match_warp<S>(cells, p, n, W, lane, list);
-            const uint32_t k = key >> 8, o = key & 255u;
-            const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
-            if (lane == 0) {
-                const T v = cell_sym<S>(cells[p]);
-                if constexpr (S == 1) {
-                    head[pl] = ptr ? uint8_t(k) : uint8_t(v);
-                    if (ptr) head[pl + 1] = uint8_t(o);
-                } else {  // pl stays even: 16-bit stores
-                    uint16_t* h16 = reinterpret_cast<uint16_t*>(head + pl);
-                    h16[0] = ptr ? uint16_t(k | (o << 8)) : uint16_t(v);
-                    if (S == 4 && !ptr) h16[1] = uint16_t(uint32_t(v) >> 16);
+        uint8_t* pay = a.pay_slots + g * uint64_t(C) * S;
+        uint32_t* fl32 = reinterpret_cast<uint32_t*>(a.flag_slots + g * uint64_t(C / 8));
+        uint32_t slot = 0, tb = 0, pl = 0, tokv = 0, nptr = 0;
+        auto flush = [&](uint32_t cnt) {
+            const bool valid = lane < cnt;
+            const bool isptr = valid && (tokv >> 31);
+            const uint32_t pm = __ballot_sync(0xffffffffu, isptr);
+            const uint32_t vm = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+            const uint32_t lm = (1u << lane) - 1u;
+            const uint32_t at = pl + 2u * __popc(pm & lm) + uint32_t(S) * __popc(vm & ~pm & lm);
+            if (valid) {
+                if (isptr) {
+                    if constexpr (S == 1) {
+                        pay[at] = uint8_t(tokv);
+                        pay[at + 1] = uint8_t(tokv >> 8);
+                    } else {
+                        *reinterpret_cast<uint16_t*>(pay + at) = uint16_t(tokv);
+                    }
+                    if (a.hist) atomicAdd(&a.hist[tokv & 0xffu], 1ull);
+                } else {
+                    const uint32_t v = uint32_t(cell_sym<S>(cells[tokv]));
+                    if constexpr (S == 1) {
+                        pay[at] = uint8_t(v);
+                    } else {
+                        *reinterpret_cast<uint16_t*>(pay + at) = uint16_t(v);
+                        if constexpr (S == 4) *reinterpret_cast<uint16_t*>(pay + at + 2) = uint16_t(v >> 16);
+                    }
                 }
             }
-            if (a.hist && ptr && lane == 0) atomicAdd(&a.hist[k], 1ull);
-            fw |= (ptr ? 1u : 0u) << ((t & 31u) ^ 7u);
-            pl += ptr ? 2u : uint32_t(S);
-            nptr += ptr ? 1u : 0u;
-            p += ptr ? static_cast<int>(k) : 1;
-            if ((t & 31u) == 31u) {
-                if (lane == 0) reinterpret_cast<uint32_t*>(flg)[t >> 5] = fw;
-                fw = 0;
+            if (lane == 0) fl32[tb >> 5] = __byte_perm(__brev(pm), 0u, 0x0123);
+            pl += 2u * __popc(pm) + uint32_t(S) * __popc(vm & ~pm);
+            nptr += __popc(pm);
+        };
+        auto push = [&](uint32_t v) {
+            if (lane == slot) tokv = v;
+            if (++slot == 32u) {
+                flush(32u);
+                slot = 0;
+                tb += 32u;
             }
-            ++t;
+        };
+        auto literals = [&](int from, int to) {
+            while (from < to) {
+                const uint32_t m = min(uint32_t(to - from), 32u - slot);
+                if (lane >= slot && lane < slot + m) tokv = uint32_t(from) + (lane - slot);
+                slot += m;
+                from += int(m);
+                if (slot == 32u) {
+                    flush(32u);
+                    slot = 0;
+                    tb += 32u;
+                }
+            }
+        };
+        int p = min(I, n);
+        literals(0, p);
+        while (p < n) {  // p is a multiple of I here
+            const uint32_t key = find_match_warp<S>(cells, p, n, W, lane, list);
+            const uint32_t k = key >> 8, o = key & 255u;
+            const bool ptr = (o != 0) && (static_cast<int>(k) >= min_match);
+            push(ptr ? (0x80000000u | k | (o << 8)) : uint32_t(p));
+            p += ptr ? static_cast<int>(k) : 1;
+            if (p & (I - 1)) {
+                const int q = min((p + I - 1) & ~(I - 1), n);
+                literals(p, q);
+                p = q;
+            }
         }
-        if ((t & 31u) != 0 && lane == 0) reinterpret_cast<uint32_t*>(flg)[t >> 5] = fw;
-        __syncwarp();
-
-        // ---- flush to the chunk's staging slots with 128-bit stores
-        const uint32_t nf = (t + 7u) >> 3;
-        uint4* dp = reinterpret_cast<uint4*>(a.pay_slots + g * uint64_t(C) * S);
-        const uint4* sp = reinterpret_cast<const uint4*>(head);
-        for (uint32_t i = lane; i < (pl + 15u) >> 4; i += 32) dp[i] = sp[i];
-        uint4* df = reinterpret_cast<uint4*>(a.flag_slots + g * uint64_t(C / 8));
-        const uint4* sf = reinterpret_cast<const uint4*>(flg);
-        for (uint32_t i = lane; i < (nf + 15u) >> 4; i += 32) df[i] = sf[i];
+        if (slot) flush(slot);
+        const uint32_t t = tb + slot;
         if (lane == 0) {
             a.psize[g] = pl;
-            a.fsize[g] = nf;
+            a.fsize[g] = (t + 7u) >> 3;
         }
         warp_ptr += nptr;
         warp_tok += t;
