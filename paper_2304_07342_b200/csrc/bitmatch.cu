@@ -224,13 +224,55 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
     return true;
 }
 
+// Which later pass takes a chunk the first pass could not hold: 0 if it has
+// at most kBmMaxSymsMid distinct symbols, 1 if at most kBmMaxSymsWide, else
+// 2.  Counts exactly (up to 65) from the input in global memory — the first
+// pass has overwritten part of its staged copy with ids.  Lane d % 32 keeps
+// distinct symbol d in tab[d / 32]; each word's new values are appended one
+// distinct value at a time.
+template <int S>
+__device__ __noinline__ int classify_alphabet(const uint8_t* src, int n, uint32_t lane) {
+    uint32_t tab[2] = {0u, 0u};
+    int D = 0;
+    for (int wi = 0; wi * 32 < n && D <= kBmMaxSymsWide; ++wi) {
+        const int i = wi * 32 + static_cast<int>(lane);
+        const bool valid = i < n;
+        uint32_t v = 0;
+        if (valid) {
+            if constexpr (S == 1) v = src[i];
+            else if constexpr (S == 2) v = uint32_t(src[2 * i]) | uint32_t(src[2 * i + 1]) << 8;
+            else v = ld_le32(src + 4 * i);
+        }
+        const uint32_t same = __match_any_sync(kFull, v) & __ballot_sync(kFull, valid);
+        uint32_t lead = __ballot_sync(kFull, valid && __ffs(same) - 1 == static_cast<int>(lane));
+        while (lead && D <= kBmMaxSymsWide) {
+            const int l = __ffs(lead) - 1;
+            lead &= lead - 1;
+            const uint32_t vl = __shfl_sync(kFull, v, l);
+            const bool hit = __any_sync(kFull, (static_cast<int>(lane) < D && tab[0] == vl) ||
+                                                   (static_cast<int>(lane) + 32 < D && tab[1] == vl));
+            if (!hit) {
+                if (D < 32) {
+                    if (static_cast<int>(lane) == D) tab[0] = vl;
+                } else if (D < 64) {
+                    if (static_cast<int>(lane) == D - 32) tab[1] = vl;
+                }
+                ++D;
+            }
+        }
+    }
+    return D <= kBmMaxSymsMid ? 0 : D <= kBmMaxSymsWide ? 1 : 2;
+}
+
 // Pass 2: occurrence rows from the ids.  Lanes holding equal ids form one
 // __match_any_sync group, whose mask IS that id's bitmap word.  Rows 0..D
-// are cleared first (row D is the all-zero row of position n).
+// are cleared first, with row D's whole reach (the all-zero row of
+// position n).
 template <int NW>
 __device__ __forceinline__ void build_rows(uint8_t* ids, int n, int D, uint32_t* rows, int RW,
                                            uint32_t lane) {
-    for (int x = static_cast<int>(lane); x < (D + 1) * RW; x += 32) rows[x] = 0u;
+    const int words = (D + 1) * RW + NW + 3;  // bm_rows_words
+    for (int x = static_cast<int>(lane); x < words; x += 32) rows[x] = 0u;
     __syncwarp();
     for (int wi = 0; wi * 32 < n; ++wi) {
         const int i = wi * 32 + static_cast<int>(lane);
@@ -295,7 +337,9 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
         uint32_t tab[(MAXS + 31) / 32];
         if (!rename_symbols<S, MAXS>(raw, n, tbl, lane, D, tab)) {
             // too many distinct symbols: the wide-cell pass takes this chunk
-            if (lane == 0) a.fb_list[atomicAdd(a.fb_count, 1u)] = uint32_t(ck);
+            const int cls = (MAXS == kBmMaxSyms && a.classify)
+                                ? classify_alphabet<S>(a.in + ck * uint64_t(C) * S, n, lane) : 0;
+            if (lane == 0) a.fb_list[cls][atomicAdd(a.fb_count[cls], 1u)] = uint32_t(ck);
             __syncwarp();
             continue;
         }

@@ -215,6 +215,8 @@ struct plzgpu_ctx {
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
     cudaStream_t copy_stream = nullptr;
     cudaStream_t asm_stream = nullptr;  // pipelined compress: per-container Kernel III
+    cudaStream_t side_stream = nullptr;  // Kernel I: the 64-row pass beside the 32-row one
+    cudaEvent_t side_ev[2] = {nullptr, nullptr};
     cudaEvent_t asm_ev[2] = {nullptr, nullptr};
     DevBuf ready;
     uint32_t epoch = 0;
@@ -331,43 +333,81 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
     e.hist = c->enc_hist;
-    // bitmap pass (16 rows) over every chunk, a bitmap pass with 64 rows over
-    // the chunks whose alphabet overflowed it, the wide-cell pass over the rest
+    // bitmap pass (16 rows) over every chunk, then the 32-row and 64-row
+    // passes over what overflowed, then the wide-cell pass.  With few chunks
+    // per resident warp the later passes' tails would add up, so the first
+    // pass then sorts its overflow by exact alphabet size and the 32- and
+    // 64-row passes run concurrently (two streams); otherwise they run one
+    // after the other, each taking the previous one's overflow.
     CK(c->fb.ensure(3 * G * 4 + 16));
     uint32_t* lists[3] = {c->fb.as<uint32_t>(), c->fb.as<uint32_t>() + G,
                           c->fb.as<uint32_t>() + 2 * G};
     uint32_t* counts[3] = {&m->work[4], &m->work[6], &m->work[8]};
-    const uint32_t* src = nullptr;
-    const uint32_t* src_n = nullptr;
     uint32_t* works[4] = {&m->work[0], &m->work[5], &m->work[9], &m->work[7]};
-    int pass = 0;
-    for (int maxsyms : {kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide}) {
+    int wpc1 = 1, per_sm1 = 0;
+    encode_shape(c, p, kBmMaxSyms, &wpc1, &per_sm1);
+    const bool classify = Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
+    e.classify = classify ? 1 : 0;
+    auto bitmap_pass = [&](int maxsyms, int pass, const uint32_t* src, const uint32_t* src_n,
+                           uint32_t* ovf, uint32_t* ovf_n, cudaStream_t s) -> bool {
         int wpc = 1, per_sm = 0;
         encode_shape(c, p, maxsyms, &wpc, &per_sm);
-        if (per_sm == 0) continue;
+        if (per_sm == 0) return false;
         EncodeArgs b = e;
         b.work = works[pass];
         b.src_list = src;
         b.src_count = src_n;
-        b.fb_list = lists[pass];
-        b.fb_count = counts[pass];
-        if (src) b.ready = nullptr;  // every segment has landed after the first pass
+        if (src) {
+            b.ready = nullptr;  // every segment has landed after the first pass
+            b.classify = 0;
+            for (int i = 0; i < 2; ++i) {
+                b.fb_list[i] = ovf;
+                b.fb_count[i] = ovf_n;
+            }
+        }
         b.warps_per_cta = wpc;
         const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (Gr + wpc - 1) / wpc);
-        launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), st);
+        launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), s);
         ++*launches;
-        src = lists[pass];
-        src_n = counts[pass];
-        ++pass;
+        return true;
+    };
+    for (int i = 0; i < 3; ++i) {
+        e.fb_list[i] = lists[i];
+        e.fb_count[i] = counts[i];
+    }
+    const uint32_t* wide_src = nullptr;
+    const uint32_t* wide_n = nullptr;
+    if (bitmap_pass(kBmMaxSyms, 0, nullptr, nullptr, nullptr, nullptr, st)) {
+        bool mid, wide;
+        if (classify) {
+            if (!c->side_stream) CK(cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+            for (cudaEvent_t& ev : c->side_ev)
+                if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(c->side_ev[0], st));
+            CK(cudaStreamWaitEvent(c->side_stream, c->side_ev[0], 0));
+            mid = bitmap_pass(kBmMaxSymsMid, 1, lists[0], counts[0], lists[2], counts[2], st);
+            wide = bitmap_pass(kBmMaxSymsWide, 2, lists[1], counts[1], lists[2], counts[2],
+                               c->side_stream);
+            CK(cudaEventRecord(c->side_ev[1], c->side_stream));
+            CK(cudaStreamWaitEvent(st, c->side_ev[1], 0));
+        } else {
+            mid = bitmap_pass(kBmMaxSymsMid, 1, lists[0], counts[0], lists[1], counts[1], st);
+            wide = bitmap_pass(kBmMaxSymsWide, 2, lists[1], counts[1], lists[2], counts[2], st);
+        }
+        if (!mid || !wide)
+            return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                           "chunk too large for the bitmap passes' shared memory");
+        wide_src = lists[2];
+        wide_n = counts[2];
     }
     {
         int wpc = 1, per_sm = 1;
         encode_shape(c, p, 0, &wpc, &per_sm);
         EncodeArgs f = e;
         f.work = works[3];
-        f.src_list = src;
-        f.src_count = src_n;
-        if (src) f.ready = nullptr;
+        f.src_list = wide_src;
+        f.src_count = wide_n;
+        if (wide_src) f.ready = nullptr;
         f.warps_per_cta = wpc;
         launch_encode(p.symbol_width, f,
                       int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1), (Gr + wpc - 1) / wpc)),
@@ -808,6 +848,12 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
         cudaStreamSynchronize(c->asm_stream);
         cudaStreamDestroy(c->asm_stream);
     }
+    if (c->side_stream) {
+        cudaStreamSynchronize(c->side_stream);
+        cudaStreamDestroy(c->side_stream);
+    }
+    for (cudaEvent_t& ev : c->side_ev)
+        if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t& ev : c->asm_ev)
         if (ev) cudaEventDestroy(ev);
     if (c->copy_stream) {

@@ -51,20 +51,26 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 //   [region: max(C*S, C + rows) + 16 bytes]
 // The region first holds the raw chunk (TMA target); pass 1 renames the
 // symbols to ids in place (bytes [0, C)); pass 2 builds the occurrence rows
-// at byte C, over the raw bytes pass 1 has consumed.  A row is the chunk's
-// C-bit occurrence bitmap of one id with NW zero words in front (windows
-// reaching before position 0) and NW + 3 behind (the search's one-round
-// look-ahead); row D (one past the chunk's last id) is all zero and is the
-// id of position n.
+// at byte C, over the raw bytes pass 1 has consumed.  Rows are strided by
+// C/32 + NW words: row r's word w (w counts NW front words, then the C-bit
+// bitmap) is rows[r * stride + w], so a row's front words are the previous
+// row's tail.  Those reads only ever feed candidate bits the search masks
+// out (w < 0 is cleared from A, bits past position n-1 fail the o >= j+1
+// mask), so their content is irrelevant — except for row D, the all-zero
+// row standing for position n, which is zeroed over its whole reach (front
+// NW words, bitmap, NW + 3 words behind: the search's one-round look-ahead).
 constexpr int kBmMaxSyms = 16;      // first bitmap pass: all chunks
 constexpr int kBmMaxSymsMid = 32;   // second bitmap pass: the first pass's overflow
 constexpr int kBmMaxSymsWide = 64;  // third bitmap pass: the second pass's overflow
 constexpr int kBmMaxThreads = 128;   // CTA size bound (registers: up to 255 per thread)
 __host__ __device__ inline int bm_nw(int W) { return W <= 32 ? 1 : W <= 64 ? 2 : W <= 128 ? 4 : 8; }
-__host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + 2 * bm_nw(W) + 3; }
+__host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + bm_nw(W); }  // stride
+__host__ __device__ inline int bm_rows_words(int C, int W, int D) {  // rows 0..D, row D's reach
+    return (D + 1) * bm_row_words(C, W) + bm_nw(W) + 3;
+}
 __host__ __device__ inline size_t bm_region(int C, int S, int W, int maxsyms) {
     const size_t raw = size_t(C) * S;
-    const size_t rows = size_t(C) + size_t(maxsyms + 1) * bm_row_words(C, W) * 4;
+    const size_t rows = size_t(C) + size_t(bm_rows_words(C, W, maxsyms)) * 4;
     return (raw > rows ? raw : rows) + 16;
 }
 __host__ __device__ inline size_t bm_warp_smem(int C, int S, int W, int maxsyms) {
@@ -96,9 +102,13 @@ struct EncodeArgs {
     // after the first), else chunks 0..n_chunks-1
     const uint32_t* src_list;
     const uint32_t* src_count;
-    // bitmap passes: chunks whose alphabet does not fit are appended here
-    uint32_t* fb_list;
-    uint32_t* fb_count;
+    // bitmap passes: chunks whose alphabet does not fit are appended to
+    // fb_list[c]: c = 0 (<= kBmMaxSymsMid symbols), 1 (<= kBmMaxSymsWide),
+    // 2 (more).  The first pass classifies its overflow exactly; the later
+    // passes only ever use fb_list[2].
+    uint32_t* fb_list[3];
+    uint32_t* fb_count[3];
+    int classify;                // first pass: sort its overflow by alphabet size (else list 0)
 };
 // the wide-cell kernel (any alphabet)
 void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);

@@ -160,6 +160,33 @@ def test_byte_alphabet_boundaries(C, W):
         assert plz.decompress_bytes(got) == data
 
 
+def test_bitmap_passes_in_sequence_on_a_large_input():
+    # Inputs with many chunks per resident warp run the 16/32/64-row bitmap
+    # passes one after the other (each takes the previous one's overflow);
+    # small inputs sort the overflow first and run the 32/64-row passes side
+    # by side.  A large input mixing alphabets of 7, 20, 40 and 100 symbols
+    # per chunk exercises the sequential order; reference image required.
+    import numpy as np
+
+    rng = np.random.default_rng(77)
+    S, C = 2, 2048
+    chunks = []
+    for k in range(20480):
+        d = (7, 20, 40, 100)[k % 4]
+        alphabet = rng.permutation(1024)[:d].astype("<u2") + 32000
+        idx = np.repeat(rng.integers(0, d, C), rng.integers(1, 4, C))[:C]
+        idx[:d] = np.arange(d)
+        chunks.append(alphabet[idx])
+    data = np.concatenate(chunks).tobytes()
+    p = P(S, 255, C, 2)
+    want, st_ref = ref_compress(data, p)
+    stats = plz.PipelineStats()
+    got = plz.compress(data, p, stats=stats)
+    assert got == want
+    assert (stats.pointer_tokens, stats.literal_tokens) == st_ref[1:]
+    assert plz.decompress_bytes(got) == data
+
+
 def test_multi_block_images():
     # test_decoder.cpp:198-207: two chunks per block, five blocks and a tail
     p = P(2, 64, 1024, 1, 1024 * 2 * 2)
