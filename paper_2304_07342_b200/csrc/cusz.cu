@@ -14,8 +14,9 @@
 //   inverse      q = Σx Σy Σz d (three axis scans), f' = float32(q) * float32(2 eb)
 //
 // |f - f'| <= eb up to float32 rounding of f * s.  HBM-bound kernels: the
-// quantizer reads each value once (the 7 Lorenzo neighbours hit L1/L2) and
-// writes 2 bytes; the scans read and write int32 once per axis.
+// quantizer reads each value once (a z-walking tile keeps the previous
+// plane's term in a register) and writes 2 bytes; the scans read and write
+// int32 once per axis.
 #include "common.cuh"
 
 namespace plzgpu {
@@ -76,30 +77,45 @@ __global__ void __launch_bounds__(kQuantThreads) plz_lorenzo_quant_kernel(
     }
 }
 
-// exclusive scan of the tile counts (one CTA; tiles are few: n / 1024)
-__global__ void __launch_bounds__(1024) plz_tile_scan_kernel(const uint32_t* __restrict__ cnt,
-                                                             uint64_t tiles, uint64_t* __restrict__ off) {
-    __shared__ uint64_t part[1024];
-    const uint64_t per = (tiles + 1023) / 1024;
-    const uint64_t b = threadIdx.x * per, e = min(tiles, b + per);
-    uint64_t s = 0;
-    for (uint64_t i = b; i < e; ++i) s += cnt[i];
-    part[threadIdx.x] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t run = 0;
-        for (int i = 0; i < 1024; ++i) {
-            const uint64_t v = part[i];
-            part[i] = run;
-            run += v;
+// 2-D / 3-D fields: a 32 x 8 thread block owns a (y, x) tile and walks it
+// through z.  Each plane's tile plus its y-1 / x-1 halo is prequantised once
+// into shared memory; a thread forms its 2-D Lorenzo term of the plane
+// (q - q_x - q_y + q_xy) and subtracts the previous plane's, kept in a
+// register — every input value is read once (+ the halo), HBM-bound.
+// Outliers bump the count of their 1024-element index tile.
+constexpr int kTileX = 32, kTileY = 8;
+
+__global__ void __launch_bounds__(kTileX * kTileY) plz_lorenzo_tiled_kernel(
+    const float* __restrict__ f, Dims g, float s, int32_t radius, uint16_t* __restrict__ codes,
+    uint32_t* __restrict__ tile_count) {
+    __shared__ int32_t qs[kTileY + 1][kTileX + 1];
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t x = int64_t(blockIdx.x) * kTileX + tx, y = int64_t(blockIdx.y) * kTileY + ty;
+    const bool in = x < int64_t(g.nx) && y < int64_t(g.ny);
+    int32_t prev = 0;  // the previous plane's 2-D term at (y, x)
+    for (uint64_t z = 0; z < g.nz; ++z) {
+        const float* plane = f + z * g.ny * g.nx;
+        // tile + halo (row y0-1, column x0-1), q = 0 outside the field
+        for (int i = ty * kTileX + tx; i < (kTileY + 1) * (kTileX + 1); i += kTileX * kTileY) {
+            const int hy = i / (kTileX + 1), hx = i % (kTileX + 1);
+            const int64_t gy = int64_t(blockIdx.y) * kTileY + hy - 1;
+            const int64_t gx = int64_t(blockIdx.x) * kTileX + hx - 1;
+            int32_t q = 0;
+            if (gy >= 0 && gx >= 0 && gy < int64_t(g.ny) && gx < int64_t(g.nx))
+                q = static_cast<int32_t>(rintf(__fmul_rn(__ldg(plane + gy * g.nx + gx), s)));
+            qs[hy][hx] = q;
         }
-        off[tiles] = run;
-    }
-    __syncthreads();
-    uint64_t run = part[threadIdx.x];
-    for (uint64_t i = b; i < e; ++i) {
-        off[i] = run;
-        run += cnt[i];
+        __syncthreads();
+        const int32_t cur = qs[ty + 1][tx + 1] - qs[ty + 1][tx] - qs[ty][tx + 1] + qs[ty][tx];
+        if (in) {
+            const int32_t d = cur - prev;
+            const uint64_t i = (z * g.ny + uint64_t(y)) * g.nx + uint64_t(x);
+            const bool ok = d > -radius && d < radius;
+            codes[i] = ok ? uint16_t(d + radius) : uint16_t(0);
+            if (!ok) atomicAdd(&tile_count[i / kQuantTile], 1u);
+        }
+        prev = cur;
+        __syncthreads();
     }
 }
 
@@ -220,12 +236,18 @@ uint64_t lorenzo_tiles(uint64_t n) { return (n + kQuantTile - 1) / kQuantTile; }
 
 void launch_lorenzo_quantize(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,
                              int32_t radius, uint16_t* codes, uint32_t* tile_count,
-                             uint64_t* tile_off, cudaStream_t st) {
+                             cudaStream_t st) {
     const uint64_t n = nx * ny * nz, tiles = lorenzo_tiles(n);
     const Dims g{nx, ny, nz};
-    plz_lorenzo_quant_kernel<<<unsigned(tiles), kQuantThreads, 0, st>>>(f, g, n, s, radius, codes,
+    if (ny > 1) {
+        cudaMemsetAsync(tile_count, 0, tiles * 4, st);
+        const dim3 grid(unsigned((nx + kTileX - 1) / kTileX), unsigned((ny + kTileY - 1) / kTileY));
+        plz_lorenzo_tiled_kernel<<<grid, dim3(kTileX, kTileY), 0, st>>>(f, g, s, radius, codes,
                                                                         tile_count);
-    plz_tile_scan_kernel<<<1, 1024, 0, st>>>(tile_count, tiles, tile_off);
+    } else {
+        plz_lorenzo_quant_kernel<<<unsigned(tiles), kQuantThreads, 0, st>>>(f, g, n, s, radius,
+                                                                            codes, tile_count);
+    }
 }
 
 void launch_outlier_write(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,

@@ -1463,11 +1463,30 @@ int plzgpu_lorenzo_quantize(plzgpu_ctx* c, const float* d_field, uint64_t nx, ui
     if (int rc = lorenzo_args(d_field, d_codes, nx, ny, nz, eb, radius, err)) return rc;
     const cudaStream_t st = pick(c, stream);
     const uint64_t n = nx * ny * nz, tiles = lorenzo_tiles(n);
-    CK(c->qtiles.ensure(tiles * 4 + 16));
-    CK(c->qoff.ensure((tiles + 1) * 8 + 16));
+    CK(c->qtiles.ensure(tiles * 4 + 64));
+    CK(c->qoff.ensure(2 * (tiles + 1) * 8 + 16));  // exclusive prefixes + a scratch twin
+    const uint64_t stiles = (tiles + kScanTile - 1) / kScanTile;
+    CK(c->status.ensure(stiles * 4 + 4));
+    CK(c->agg.ensure(stiles * 16 + 16));
+    CK(c->incl.ensure(stiles * 16 + 16));
     const float s = float(1.0 / (2.0 * eb));
-    launch_lorenzo_quantize(d_field, nx, ny, nz, s, radius, d_codes, c->qtiles.as<uint32_t>(),
-                            c->qoff.as<uint64_t>(), st);
+    launch_lorenzo_quantize(d_field, nx, ny, nz, s, radius, d_codes, c->qtiles.as<uint32_t>(), st);
+    // exclusive scan of the per-tile counts: Kernel II (the flag half of its
+    // pair scan runs on the same counts into a scratch twin)
+    Meta* m = dmeta(c);
+    CK(cudaMemsetAsync(c->status.p, 0, stiles * 4, st));
+    CK(cudaMemsetAsync(&m->work[1], 0, 4, st));
+    ScanArgs sa{};
+    sa.psize = c->qtiles.as<uint32_t>();
+    sa.fsize = c->qtiles.as<uint32_t>();
+    sa.n = tiles;
+    sa.P64 = c->qoff.as<uint64_t>();
+    sa.F64 = c->qoff.as<uint64_t>() + tiles + 1;
+    sa.status = c->status.as<uint32_t>();
+    sa.agg = c->agg.as<ulonglong2>();
+    sa.incl = c->incl.as<ulonglong2>();
+    sa.tile_counter = &m->work[1];
+    launch_scan(sa, st);
     launch_outlier_write(d_field, nx, ny, nz, s, d_codes, c->qtiles.as<uint32_t>(),
                          c->qoff.as<uint64_t>(), d_outlier_idx, d_outlier_val, outlier_cap, st);
     CK(cudaGetLastError());

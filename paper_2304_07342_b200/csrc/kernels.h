@@ -273,10 +273,11 @@ void launch_mono_detail(const DecodeArgs& a, unsigned long long key, uint64_t* b
 
 // ------------------------------------------------ cuSZ dual quantization
 uint64_t lorenzo_tiles(uint64_t n);
-// codes + per-tile outlier counts + their exclusive scan (tile_off[tiles] = total)
+// codes + per-tile (1024 elements) outlier counts; the host scans the counts
+// with Kernel II (launch_scan) before launch_outlier_write
 void launch_lorenzo_quantize(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,
                              int32_t radius, uint16_t* codes, uint32_t* tile_count,
-                             uint64_t* tile_off, cudaStream_t st);
+                             cudaStream_t st);
 void launch_outlier_write(const float* f, uint64_t nx, uint64_t ny, uint64_t nz, float s,
                           const uint16_t* codes, const uint32_t* tile_count,
                           const uint64_t* tile_off, uint64_t* out_idx, int32_t* out_val,
