@@ -287,7 +287,8 @@ void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int* wpc_o
 // [g0, g1) of the G; their prefixes continue from P64/F64[g0].
 int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t G,
                         uint32_t last_len, cudaStream_t st, plzgpu_error* err, int* launches,
-                        bool scan = true, uint64_t g0 = 0, uint64_t g1 = UINT64_MAX) {
+                        bool scan = true, uint64_t g0 = 0, uint64_t g1 = UINT64_MAX,
+                        bool side_passes = true) {
     const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size);
     if (g1 > G) g1 = G;
     const uint64_t Gr = g1 - g0;  // chunks of this call
@@ -346,7 +347,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     uint32_t* works[4] = {&m->work[0], &m->work[5], &m->work[9], &m->work[7]};
     int wpc1 = 1, per_sm1 = 0;
     encode_shape(c, p, kBmMaxSyms, &wpc1, &per_sm1);
-    const bool classify = Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
+    const bool classify = side_passes && Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
     e.classify = classify ? 1 : 0;
     auto bitmap_pass = [&](int maxsyms, int pass, const uint32_t* src, const uint32_t* src_n,
                            uint32_t* ovf, uint32_t* ovf_n, cudaStream_t s) -> bool {
@@ -366,7 +367,10 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
             }
         }
         b.warps_per_cta = wpc;
-        const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * per_sm, (Gr + wpc - 1) / wpc);
+        // a pipelined compress leaves one CTA slot per SM for the previous
+        // container's Kernel III on the assembly stream
+        const int resident = side_passes ? per_sm : std::max(1, per_sm - 1);
+        const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * resident, (Gr + wpc - 1) / wpc);
         launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), s);
         ++*launches;
         return true;
@@ -500,8 +504,10 @@ int enqueue_compress_by_container(plzgpu_ctx* c, const plzgpu_params& p, const u
     int launches = 0;
     for (uint64_t j = 0; j < g.n_blocks; ++j) {
         const uint64_t g0 = j * g.cpb, g1 = std::min(g.n_chunks, g0 + g.cpb);
+        // (no side-stream passes here: Kernel III of the previous container
+        // is running on the assembly stream)
         int rc = enqueue_encode_scan(c, p, d_in, g.n_chunks, g.last_len, st, err, &launches, true,
-                                     g0, g1);
+                                     g0, g1, false);
         if (rc) return rc;
         CK(cudaEventRecord(c->asm_ev[0], st));
         CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
