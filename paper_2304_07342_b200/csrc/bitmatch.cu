@@ -281,7 +281,9 @@ __device__ __forceinline__ void build_rows(uint8_t* ids, int n, int D, uint32_t*
         const uint32_t same = __match_any_sync(kFull, id);
         if (valid && __ffs(same) - 1 == static_cast<int>(lane)) rows[id * RW + NW + wi] = same;
     }
-    if (lane == 0) ids[n] = uint8_t(D);
+    // positions n .. n + 127 read the all-zero row D (steps past the chunk end
+    // fail; the search's look-ahead reaches at most 3G - 1 <= 95 past n)
+    for (int i = static_cast<int>(lane); i < kBmIdPad; i += 32) ids[n + i] = uint8_t(D);
     __syncwarp();
 }
 
@@ -301,7 +303,7 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     uint2* tbl = reinterpret_cast<uint2*>(base + 16);
     uint8_t* raw = base + 16 + 2 * MAXS * 8;
     uint8_t* ids = raw;
-    uint32_t* rows = reinterpret_cast<uint32_t*>(raw + C);
+    uint32_t* rows = reinterpret_cast<uint32_t*>(raw + C + kBmIdPad);
 
     if (lane == 0) mbar_init(mbar, 1);
     __syncwarp();
@@ -375,25 +377,23 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
             uint32_t K = 0, off = 0;
             {
                 // bit b of word jw <-> candidate w = p - W + 32*jw + b.
-                // Step k + grp reads the id of position p + k + grp (clamped
-                // to n: the zero row) and the row bits from p + qc + k; the
-                // next round's ids are loaded a round ahead.
+                // Step k + grp reads the id of position p + k + grp (the ids
+                // past n are D: the zero row) and the row bits from
+                // p + qc + k; the next round's ids are loaded a round ahead.
                 uint32_t A = shl_clamp(kFull, uint32_t(max(lbc - p, 0)));
                 uint32_t x, nz;
-                const uint32_t ib = s_ids + uint32_t(p + grp);
-                const int lim = n - p - grp;
                 int q = p + qc;               // row bit cursor (advances G per round)
                 const int mk = clg - q;       // mask shift of the round: max(mk + q, 0)
-                const int ik = lim + q;       // id index clamp: min(q - q0, lim) = min(q, ik) - q0
+                const uint32_t ib = s_ids + uint32_t(p + grp) - uint32_t(q);  // + q: step's id
                 const int q0 = q;
-                uint32_t id = lds_u8(ib + uint32_t(min(0, lim)));
-                uint32_t idn = lds_u8(ib + uint32_t(min(G, lim)));
+                uint32_t id = lds_u8(ib + uint32_t(q));
+                uint32_t idn = lds_u8(ib + uint32_t(q + G));
 #pragma unroll 2
                 for (;;) {
                     const uint32_t ra = s_rows + id * uint32_t(RW * 4) + uint32_t((q >> 5) << 2);
                     const uint32_t lo = lds_u32(ra), hi = lds_u32(ra + 4);
                     id = idn;
-                    idn = lds_u8(ib + uint32_t(min(q + 2 * G, ik) - q0));
+                    idn = lds_u8(ib + uint32_t(q + 2 * G));
                     const uint32_t f = __funnelshift_r(lo, hi, uint32_t(q));
                     x = f & shr_clamp(kFull, uint32_t(max(mk + q, 0))) & A;
 #pragma unroll

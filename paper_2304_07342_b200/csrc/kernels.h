@@ -50,8 +50,9 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 //   [mbarrier 16][id hash table: 2*maxsyms x {key, id} u32 pairs]
 //   [region: max(C*S, C + rows) + 16 bytes]
 // The region first holds the raw chunk (TMA target); pass 1 renames the
-// symbols to ids in place (bytes [0, C)); pass 2 builds the occurrence rows
-// at byte C, over the raw bytes pass 1 has consumed.  Rows are strided by
+// symbols to ids in place (bytes [0, C), then D up to byte n + 127); pass 2
+// builds the occurrence rows at byte C + 128, over the raw bytes pass 1 has
+// consumed.  Rows are strided by
 // C/32 + NW words: row r's word w (w counts NW front words, then the C-bit
 // bitmap) is rows[r * stride + w], so a row's front words are the previous
 // row's tail.  Those reads only ever feed candidate bits the search masks
@@ -68,9 +69,10 @@ __host__ __device__ inline int bm_row_words(int C, int W) { return C / 32 + bm_n
 __host__ __device__ inline int bm_rows_words(int C, int W, int D) {  // rows 0..D, row D's reach
     return (D + 1) * bm_row_words(C, W) + bm_nw(W) + 3;
 }
+constexpr int kBmIdPad = 128;  // ids[n .. n+127] = D: the search reads ids unclamped
 __host__ __device__ inline size_t bm_region(int C, int S, int W, int maxsyms) {
     const size_t raw = size_t(C) * S;
-    const size_t rows = size_t(C) + size_t(bm_rows_words(C, W, maxsyms)) * 4;
+    const size_t rows = size_t(C) + kBmIdPad + size_t(bm_rows_words(C, W, maxsyms)) * 4;
     return (raw > rows ? raw : rows) + 16;
 }
 __host__ __device__ inline size_t bm_warp_smem(int C, int S, int W, int maxsyms) {
