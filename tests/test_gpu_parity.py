@@ -187,6 +187,32 @@ def test_bitmap_passes_in_sequence_on_a_large_input():
     assert plz.decompress_bytes(got) == data
 
 
+def test_concurrent_host_threads_give_identical_images():
+    # SPEC: calls are pure functions, safe on distinct buffers from several
+    # threads (one context per host thread); images must not depend on it.
+    import threading
+
+    inputs_ = [inputs.make(k, 300000 + 7 * i, 40 + i, 2) for i, k in
+               enumerate(("quant", "runs", "alpha", "uniform", "quant", "periodic"))]
+    p = P(2, 255, 2048, 2, 2048 * 2 * 16)
+    want = [plz.compress(d, p) for d in inputs_]
+    got = [None] * len(inputs_)
+    back = [None] * len(inputs_)
+
+    def work(i):
+        for _ in range(3):
+            got[i] = plz.compress(inputs_[i], p)
+            back[i] = plz.decompress_bytes(got[i])
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(inputs_))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert got == want
+    assert back == inputs_
+
+
 def test_multi_block_images():
     # test_decoder.cpp:198-207: two chunks per block, five blocks and a tail
     p = P(2, 64, 1024, 1, 1024 * 2 * 2)
