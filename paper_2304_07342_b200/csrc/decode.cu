@@ -310,18 +310,17 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
                 const int tv = int(lds32(s_tb + 4u * (before + __popc(starts & upto))));
                 // batch-relative source; negative = an earlier batch (final)
                 int src = q + tv;
-                bool more = tv != 0 && src >= int(w << 5) && q < int(span);
-                if (__any_sync(0xffffffffu, more)) {
-                    // a source in this wave: chase it back to a literal or an
-                    // earlier wave
+                if (__any_sync(0xffffffffu, tv != 0 && src >= int(w << 5))) {
+                    // sources inside the wave: pointer jumping over the lanes —
+                    // a lane whose source is lane r's position takes lane r's
+                    // source (a literal lane's source is itself), until every
+                    // source is final (a literal or an earlier wave)
+                    bool more;
                     do {
-                        if (more) {
-                            const uint32_t i = uint32_t(src) & 31u;
-                            const int t2 = int(lds32(
-                                s_tb + 4u * (before + __popc(starts & ((2u << i) - 1u)))));
-                            src += t2;
-                            more = t2 != 0 && src >= int(w << 5);
-                        }
+                        const bool in = src >= int(w << 5);
+                        const int s2 = __shfl_sync(0xffffffffu, src, uint32_t(src) & 31u);
+                        more = in && s2 != src;
+                        src = in ? s2 : src;
                     } while (__any_sync(0xffffffffu, more));
                 }
                 sts_sym<S>(s_w + uint32_t(q) * S, lds_sym<S>(uint32_t(int(s_w) + src * S)));
