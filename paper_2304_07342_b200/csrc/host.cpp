@@ -210,7 +210,7 @@ struct plzgpu_ctx {
     DecodeArgs last_decode{};
     int enc_wpc[2240] = {};  // launch shape cache per (pass, S, C)
     int enc_ctas[2240] = {};
-    DevBuf fb;               // chunks the bitmap pass left to the wide pass
+    DevBuf fb;               // overflow lists of the bitmap passes (3 x G chunk indices)
     DevBuf shard_desc;        // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
     cudaStream_t copy_stream = nullptr;

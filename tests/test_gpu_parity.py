@@ -102,7 +102,7 @@ def test_configs_bit_exact(S, W, C, I, kind):
 
 
 @pytest.mark.parametrize("S,C", [(2, 2048), (2, 1024), (4, 1024), (4, 4096)])
-def test_symbol_dictionary_boundary(S, C):
+def test_alphabet_tier_boundaries(S, C):
     # Kernel I's bitmap passes keep one occurrence row per distinct symbol of
     # a chunk (at most 16, then 32, then 64); chunks with more go to the
     # wide-cell pass.  Chunks with 1, 3, 7, 15-17, 31-33, 63-65, 255-257 and
