@@ -385,6 +385,7 @@ def run_b200(args):
     ev[1].record(stream)
     torch.cuda.synchronize()
     e2e_c_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
+    h_out.zero_()
     barrier()
     ev[0].record(stream)
     for _ in range(args.steps):
@@ -393,6 +394,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     e2e_d_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
     e2e_ok = bytes(h_img[:n_img].numpy().tobytes()) == bytes(img[:n_img].cpu().numpy().tobytes())
+    e2e_dec_ok = bool(torch.equal(h_out, h_in))
 
     if rank != 0:
         if world > 1:
@@ -431,7 +433,8 @@ def run_b200(args):
                 "h2d_bytes_per_step": n, "d2h_bytes_per_step": n_img,
                 "matches_device_image": e2e_ok,
                 "decompress": {"value": total_in / (e2e_d_ms * 1e-3) / 1e9, "unit": "GB/s",
-                               "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n}},
+                               "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n,
+                               "roundtrip_ok": e2e_dec_ok}},
         "roofline": {"kernel": "plz_bitmatch_kernel (Kernel I, bitmap pass)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,

@@ -177,4 +177,11 @@ void launch_headers(const AssembleArgs& a, cudaStream_t st) {
     plz_headers_kernel<<<unsigned((nj + 127) / 128), 128, 0, st>>>(a);
 }
 
+void preload_assemble_kernels() {
+    preload_kernel(reinterpret_cast<const void*>(plz_assemble_kernel));
+    preload_kernel(reinterpret_cast<const void*>(plz_headers_kernel));
+    preload_kernel(reinterpret_cast<const void*>(plz_shard_assemble_kernel));
+    preload_kernel(reinterpret_cast<const void*>(plz_shard_headers_kernel));
+}
+
 }  // namespace plzgpu

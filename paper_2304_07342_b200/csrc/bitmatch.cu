@@ -493,4 +493,10 @@ void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStre
     cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
+void preload_bitmatch_kernels() {
+    for (int S : {1, 2, 4})
+        for (int W : {16, 48, 96, 255})
+            for (int m : {kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide}) preload_kernel(bitmatch_fn(S, W, m));
+}
+
 }  // namespace plzgpu

@@ -280,4 +280,17 @@ void launch_lorenzo_reconstruct(const uint16_t* codes, const uint64_t* out_idx,
     }
 }
 
+void preload_cusz_kernels() {
+    const void* fs[] = {reinterpret_cast<const void*>(plz_codes_to_delta_kernel),
+                          reinterpret_cast<const void*>(plz_dequant_kernel),
+                          reinterpret_cast<const void*>(plz_lorenzo_quant_kernel),
+                          reinterpret_cast<const void*>(plz_lorenzo_tiled_kernel),
+                          reinterpret_cast<const void*>(plz_outlier_scatter_kernel),
+                          reinterpret_cast<const void*>(plz_outlier_write_kernel),
+                          reinterpret_cast<const void*>(plz_scan_strided_kernel<false>),
+                          reinterpret_cast<const void*>(plz_scan_strided_kernel<true>),
+                          reinterpret_cast<const void*>(plz_scan_x_kernel)};
+    for (const void* f : fs) preload_kernel(f);
+}
+
 }  // namespace plzgpu

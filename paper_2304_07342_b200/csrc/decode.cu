@@ -576,6 +576,27 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
 }
 
 // ----------------------------------------------------------------- decode
+// Pipelined host image: waits (lane 0, bounded ~4 s) until the H2D segment
+// holding image byte `b` has landed; all earlier segments land before it.
+// bar.warp.sync in the broadcast orders the other lanes' later loads.
+__device__ __forceinline__ bool wait_image(const DecodeArgs& a, uint64_t b, uint32_t lane) {
+    if (!a.in_ready) return true;
+    uint32_t ok = 1;
+    if (lane == 0) {
+        const uint32_t* f = a.in_ready + b / a.in_seg;
+        const long long t0 = clock64();
+        while (ld_acquire_sys(f) != a.epoch) {
+            __nanosleep(256);
+            if (clock64() - t0 > (1ll << 33)) {
+                atomicExch(a.stalled, 1u);
+                ok = 0;
+                break;
+            }
+        }
+    }
+    return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
+
 template <int S>
 __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const ContainerDesc& d,
                                                      uint64_t k, uint8_t* stage, uint32_t lane,
@@ -583,6 +604,10 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     // table entries k, k+1 of both tables: lanes 0-7 payload, 8-15 flags
     const uint8_t* ptab = a.img + d.img_off + 26;
     const uint8_t* ftab = ptab + 4 * (uint64_t(d.num_chunks) + 1);
+    if (!wait_image(a, uint64_t(ftab - a.img) + 4 * k + 7, lane)) {
+        *err_tok = 0;
+        return TE_OK;  // stalled: the host reports it
+    }
     uint32_t byte = 0;
     if (lane < 8) byte = ptab[4 * k + lane];
     else if (lane < 16) byte = ftab[4 * k + (lane - 8)];
@@ -602,6 +627,11 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     // an entry past its stream's end implies a decrease further on (the last
     // entry is the stream size): skip, the violating chunk reports it
     if (p1 > d.payload_len || f1 > d.payload_off - d.flags_off) {
+        *err_tok = 0;
+        return TE_OK;
+    }
+    // the chunk's streams plus the decoder's read-ahead slack
+    if (!wait_image(a, min(d.payload_off + p1 + 127, a.img_len - 1), lane)) {
         *err_tok = 0;
         return TE_OK;
     }
@@ -680,6 +710,23 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArg
         uint64_t k, tok;
         const uint32_t e = decode_global_chunk(a, g, stage, lane, &k, &tok);
         if (e != TE_OK && lane == 0) atomicMin(a.err_chunk, (unsigned long long)g);
+        if (a.out_done) {
+            // counted whatever the outcome (the D2H stream must never wait
+            // forever); a failed call is re-run on the resident path
+            __threadfence_system();
+            __syncwarp();
+            if (lane == 0) {
+                const ContainerDesc& d = a.desc[find_container(a.desc, a.result->n_containers, g)];
+                const uint64_t CS = uint64_t(d.chunk_size) * d.S;
+                const uint64_t o0 = d.out_off + k * CS;
+                const uint64_t o1 = o0 + (k + 1 == d.num_chunks ? uint64_t(d.last_len) * d.S : CS);
+                for (uint64_t sg = o0 / a.out_seg; sg * a.out_seg < o1; ++sg) {
+                    const uint64_t lo = max(o0, sg * a.out_seg);
+                    const uint64_t hi = min(o1, (sg + 1) * a.out_seg);
+                    atomicAdd(a.out_done + sg, uint32_t(hi - lo));
+                }
+            }
+        }
     }
 }
 
@@ -770,6 +817,15 @@ void launch_mono_detail(const DecodeArgs& a, unsigned long long key, uint64_t* b
 
 void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {
     plz_decode_one_kernel<<<1, 32, 0, st>>>(a);
+}
+
+void preload_decode_kernels() {
+    for (const void* f : {reinterpret_cast<const void*>(plz_parse_kernel),
+                          reinterpret_cast<const void*>(plz_decode_kernel),
+                          reinterpret_cast<const void*>(plz_chunk_detail_kernel),
+                          reinterpret_cast<const void*>(plz_mono_detail_kernel),
+                          reinterpret_cast<const void*>(plz_decode_one_kernel)})
+        preload_kernel(f);
 }
 
 }  // namespace plzgpu

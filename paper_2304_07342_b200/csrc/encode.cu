@@ -569,4 +569,11 @@ void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
     cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
+void preload_encode_kernels() {
+    for (int S : {1, 2, 4}) preload_kernel(encode_kernel_for(S));
+    preload_kernel(reinterpret_cast<const void*>(plz_match_table_kernel<1>));
+    preload_kernel(reinterpret_cast<const void*>(plz_match_table_kernel<2>));
+    preload_kernel(reinterpret_cast<const void*>(plz_match_table_kernel<4>));
+}
+
 }  // namespace plzgpu

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -218,7 +219,7 @@ struct plzgpu_ctx {
     cudaStream_t side_stream = nullptr;  // Kernel I: the 64-row pass beside the 32-row one
     cudaEvent_t side_ev[2] = {nullptr, nullptr};
     cudaEvent_t asm_ev[2] = {nullptr, nullptr};
-    DevBuf ready;
+    DevBuf ready, done;
     uint32_t epoch = 0;
     const uint32_t* pipe_ready = nullptr;  // set while enqueueing a pipelined encode
     uint32_t pipe_seg_chunks = 0;
@@ -303,8 +304,11 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     CK(c->agg.ensure(tiles * 16 + 16));
     CK(c->incl.ensure(tiles * 16 + 16));
     Meta* m = dmeta(c);
-    if (g0 == 0) CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
-    CK(cudaMemsetAsync(m->work, 0, sizeof m->work + sizeof m->stalled, st));
+    if (g0 == 0) {  // once per call: a later container must not clear an earlier stall
+        CK(cudaMemsetAsync(&m->stats, 0, sizeof m->stats + sizeof m->overflow, st));
+        CK(cudaMemsetAsync(&m->stalled, 0, sizeof m->stalled, st));
+    }
+    CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
     if (G == 0) {
         CK(cudaMemsetAsync(c->p64.p, 0, 8, st));
         CK(cudaMemsetAsync(c->f64.p, 0, 8, st));
@@ -681,6 +685,199 @@ int finish_decompress(plzgpu_ctx* c, cudaStream_t st, bool* grow, plzgpu_error* 
     return PLZGPU_OK;
 }
 
+// Every kernel loaded once per device (see preload_kernel in kernels.h).
+void preload_kernels(int device) {
+    static std::mutex mu;
+    static std::vector<int> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (std::find(done.begin(), done.end(), device) != done.end()) return;
+    preload_bitmatch_kernels();
+    preload_encode_kernels();
+    preload_scan_kernels();
+    preload_assemble_kernels();
+    preload_decode_kernels();
+    preload_cusz_kernels();
+    done.push_back(device);
+}
+
+// cuStreamWaitValue32 (CU_STREAM_WAIT_VALUE_GEQ = 0) through the entry point.
+typedef int (*StreamWaitValue32Fn)(void* stream, unsigned long long addr, uint32_t value,
+                                   unsigned int flags);
+StreamWaitValue32Fn stream_wait_value32() {
+    static StreamWaitValue32Fn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<StreamWaitValue32Fn>(p);
+    }();
+    return fn;
+}
+
+uint32_t host_le32(const uint8_t* b) {
+    return uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+}
+
+// Host image -> pinned host output, all three legs overlapped: the image
+// goes up in segments (copy_stream, ready flags as in plzgpu_compress), the
+// decode kernel waits per chunk for the segment its streams end in, and
+// each decoded output segment goes down (asm_stream) as soon as the kernel
+// has counted all of its bytes.  The container walk runs on the host over
+// the caller's image; anything it does not accept as well-formed — and any
+// error the kernel sees — falls back to the resident path, which reports
+// the reference's exact error.  Returns 1 when it produced the output.
+int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, uint8_t* out,
+                             uint64_t cap, uint64_t* out_len, cudaStream_t st,
+                             plzgpu_error* err) {
+    const uint64_t seg_in = 16ull << 20, seg_out = 32ull << 20;
+    StreamWriteValue32Fn write_value = stream_write_value32();
+    StreamWaitValue32Fn wait_value = stream_wait_value32();
+    if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC")) return 0;
+    // the container walk (format.cpp:112-185 on a well-formed image)
+    std::vector<ContainerDesc> descs;
+    uint64_t at = 0, total_out = 0, total_chunks = 0;
+    while (at < len) {
+        const uint8_t* b = img + at;
+        const uint64_t size = len - at;
+        if (size < 26 || b[0] != 'P' || b[1] != 'L' || b[2] != 'Z' || b[3] != '1' || b[4] != 1 ||
+            b[8] != 0)
+            return 0;
+        const uint32_t S = b[5], W = b[6], I = b[7], C = host_le32(b + 9);
+        if ((S != 1 && S != 2 && S != 4) || W < 4 || W > 255 || C <= W ||
+            (C != 1024 && C != 2048 && C != 4096 && C != 8192 && C != 16384) ||
+            (I != 1 && I != 2 && I != 4 && I != 8 && I != 16) || b[25] >= S)
+            return 0;
+        const uint64_t n = host_le32(b + 21), tail = b[25];
+        if (size < 26 + 8 * (n + 1)) return 0;
+        const uint8_t* ptab = b + 26;
+        const uint8_t* ftab = ptab + 4 * (n + 1);
+        const uint64_t ptot = host_le32(ptab + 4 * n), ftot = host_le32(ftab + 4 * n);
+        const uint64_t orig = uint64_t(host_le32(b + 13)) | uint64_t(host_le32(b + 17)) << 32;
+        const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + tail;
+        if (host_le32(ptab) != 0 || host_le32(ftab) != 0 || size < need || orig < tail ||
+            (orig - tail) % S != 0 || ((orig - tail) / S + C - 1) / C != n ||
+            total_out + orig > cap)
+            return 0;
+        ContainerDesc d{};
+        d.img_off = at;
+        d.out_off = total_out;
+        d.chunk_base = total_chunks;
+        d.flags_off = at + 26 + 8 * (n + 1);
+        d.payload_off = d.flags_off + ftot;
+        d.payload_len = ptot;
+        d.original_len = orig;
+        d.num_chunks = uint32_t(n);
+        d.chunk_size = C;
+        d.last_len = n ? uint32_t((orig - tail) / S - (n - 1) * C) : 0u;
+        d.S = uint8_t(S);
+        d.W = uint8_t(W);
+        d.I = uint8_t(I);
+        d.tail_len = uint8_t(tail);
+        descs.push_back(d);
+        at += need;
+        total_out += orig;
+        total_chunks += n;
+    }
+    if (descs.empty() || total_chunks == 0) return 0;
+    const uint64_t nseg_in = (len + seg_in - 1) / seg_in;
+    const uint64_t nseg_out = (total_out + seg_out - 1) / seg_out;
+    if (nseg_in < 2 && nseg_out < 2) return 0;  // nothing to overlap
+    // decoded bytes each output segment receives from chunks (tails excluded)
+    std::vector<uint32_t> expect(nseg_out, 0);
+    for (const ContainerDesc& d : descs) {
+        const uint64_t o0 = d.out_off, o1 = d.out_off + d.original_len - d.tail_len;
+        for (uint64_t sg = o0 / seg_out; sg * seg_out < o1; ++sg)
+            expect[sg] += uint32_t(std::min(o1, (sg + 1) * seg_out) - std::max(o0, sg * seg_out));
+    }
+    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (!c->asm_stream) CK(cudaStreamCreateWithFlags(&c->asm_stream, cudaStreamNonBlocking));
+    if (!c->asm_ev[0]) {
+        CK(cudaEventCreateWithFlags(&c->asm_ev[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->asm_ev[1], cudaEventDisableTiming));
+    }
+    CK(c->img.ensure(len + 16));
+    CK(c->out.ensure(total_out + 16));
+    CK(c->ready.ensure(nseg_in * 4));
+    CK(c->done.ensure(nseg_out * 4));
+    CK(c->desc.ensure(std::max<uint64_t>(descs.size(), 64) * sizeof(ContainerDesc)));
+    Meta* m = dmeta(c);
+    ++c->epoch;
+    if (c->epoch == 0) {  // never reuse the initial 0 flags
+        CK(cudaMemsetAsync(c->ready.p, 0, nseg_in * 4, st));
+        ++c->epoch;
+    }
+    ParseResult pr{};
+    pr.n_containers = descs.size();
+    pr.total_chunks = total_chunks;
+    pr.total_out = total_out;
+    CK(cudaMemcpyAsync(c->desc.p, descs.data(), descs.size() * sizeof(ContainerDesc),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(&m->parse, &pr, sizeof pr, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk + sizeof m->mono_key, st));
+    CK(cudaMemsetAsync(m->work, 0, sizeof m->work + sizeof m->stalled, st));
+    CK(cudaMemsetAsync(c->done.p, 0, nseg_out * 4, st));
+    CK(cudaEventRecord(c->asm_ev[0], st));
+    DecodeArgs a{};
+    a.img = c->img.as<uint8_t>();
+    a.img_len = len;
+    a.out = c->out.as<uint8_t>();
+    a.out_cap = cap;
+    a.desc = c->desc.as<ContainerDesc>();
+    a.desc_cap = c->desc.cap / sizeof(ContainerDesc);
+    a.result = &m->parse;
+    a.err_chunk = &m->err_chunk;
+    a.mono_key = &m->mono_key;
+    a.work = &m->work[2];
+    a.in_ready = c->ready.as<uint32_t>();
+    a.epoch = c->epoch;
+    a.stalled = &m->stalled;
+    a.in_seg = seg_in;
+    a.out_done = c->done.as<uint32_t>();
+    a.out_seg = seg_out;
+    int per_sm = decode_ctas_per_sm();
+    if (per_sm < 1) per_sm = 1;
+    launch_decode(a, c->sms * per_sm, st);
+    CK(cudaGetLastError());
+    // the image up, segment by segment, after the flags' reset above
+    CK(cudaStreamWaitEvent(c->copy_stream, c->asm_ev[0], 0));
+    for (uint64_t sg = 0; sg < nseg_in; ++sg) {
+        const uint64_t lo = sg * seg_in, hi = std::min(len, lo + seg_in);
+        CK(cudaMemcpyAsync(c->img.as<uint8_t>() + lo, img + lo, hi - lo, cudaMemcpyHostToDevice,
+                           c->copy_stream));
+        if (write_value(c->copy_stream, reinterpret_cast<unsigned long long>(a.in_ready + sg),
+                        c->epoch, 0) != 0)
+            return 0;
+    }
+    // the output down, each segment once its decoded bytes are counted
+    CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
+    for (uint64_t sg = 0; sg < nseg_out; ++sg) {
+        if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(a.out_done + sg),
+                       expect[sg], 0) != 0)
+            return 0;
+        const uint64_t lo = sg * seg_out, hi = std::min(total_out, lo + seg_out);
+        CK(cudaMemcpyAsync(out + lo, a.out + lo, hi - lo, cudaMemcpyDeviceToHost, c->asm_stream));
+    }
+    CK(cudaEventRecord(c->asm_ev[1], c->asm_stream));
+    CK(cudaStreamWaitEvent(st, c->asm_ev[1], 0));
+    Meta* h = c->host_meta;
+    CK(cudaMemcpyAsync(h, m, sizeof(Meta), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaStreamSynchronize(c->copy_stream));
+    c->last_launches = 1;
+    c->last_op = OP_DECOMPRESS;
+    c->last_decode = a;
+    if (h->stalled || h->err_chunk != ~0ull || h->mono_key != ~0ull) return 0;
+    // raw tails straight from the image (decoder.cpp:123-125)
+    for (const ContainerDesc& d : descs)
+        if (d.tail_len)
+            std::memcpy(out + d.out_off + d.original_len - d.tail_len,
+                        img + d.payload_off + d.payload_len, d.tail_len);
+    *out_len = total_out;
+    return 1;
+}
+
 }  // namespace
 
 // =================================================================== C-ABI
@@ -832,6 +1029,7 @@ int plzgpu_ctx_create(int device, plzgpu_ctx** out, plzgpu_error* err) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = c->meta.ensure(sizeof(Meta));
     if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_meta), sizeof(Meta));
+    if (e == cudaSuccess) preload_kernels(device);
     if (e != cudaSuccess) {
         plzgpu_ctx_destroy(c);
         return cuda_fail(err, e, "plzgpu_ctx_create");
@@ -867,6 +1065,7 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
         cudaStreamDestroy(c->copy_stream);
     }
     c->ready.release();
+    c->done.release();
     c->shard_desc.release();
     delete c;
 }
@@ -1023,6 +1222,11 @@ int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, u
     CK(cudaSetDevice(c->device));
     const cudaStream_t st = pick(c, stream);
     const uint8_t* d_img = static_cast<const uint8_t*>(img);
+    if (!is_device_ptr(img) && is_pinned_host(out) &&
+        try_decompress_pipelined(c, static_cast<const uint8_t*>(img), len,
+                                 static_cast<uint8_t*>(out), cap, out_len, st, err) == 1)
+        return PLZGPU_OK;
+    clear_err(err);  // the resident path below reports any error
     if (!is_device_ptr(img)) {
         CK(c->img.ensure(len));
         CK(cudaMemcpyAsync(c->img.p, img, len, cudaMemcpyHostToDevice, st));

@@ -249,6 +249,16 @@ struct DecodeArgs {
     // first table-monotonicity violation (global chunk << 1 | flag table),
     // ~0 if none; null: not checked (size-only walks)
     unsigned long long* mono_key;
+    // optional H2D/D2H pipeline of host buffers (plzgpu_decompress): image
+    // byte b may be read once in_ready[b / in_seg] == epoch; each chunk adds
+    // its decoded bytes to out_done[o / out_seg] for every output segment it
+    // covers once they are written (the D2H stream waits on those counts)
+    const uint32_t* in_ready;
+    uint32_t epoch;
+    uint32_t* stalled;
+    uint64_t in_seg;
+    uint32_t* out_done;
+    uint64_t out_seg;
 };
 void launch_parse(const DecodeArgs& a, cudaStream_t st);
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
@@ -256,6 +266,22 @@ void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st);
 int decode_ctas_per_sm();
+
+// Lazy module loading (the CUDA 12 default) loads a kernel at its first
+// launch, and that load waits for the device's running work: a launch queued
+// behind a kernel that spins on H2D segments the host has not enqueued yet
+// would stall the pipeline.  Each file's kernels are loaded up front instead
+// (cudaFuncGetAttributes forces the load).
+inline void preload_kernel(const void* f) {
+    cudaFuncAttributes at;
+    if (cudaFuncGetAttributes(&at, f) != cudaSuccess) (void)cudaGetLastError();
+}
+void preload_assemble_kernels();
+void preload_scan_kernels();
+void preload_cusz_kernels();
+void preload_decode_kernels();
+void preload_encode_kernels();
+void preload_bitmatch_kernels();
 
 struct DecodeOneArgs {
     const uint8_t* flags;

@@ -163,4 +163,6 @@ void launch_scan(const ScanArgs& a, cudaStream_t st) {
     plz_scan_kernel<<<unsigned(tiles), kScanThreads, 0, st>>>(a);
 }
 
+void preload_scan_kernels() { preload_kernel(reinterpret_cast<const void*>(plz_scan_kernel)); }
+
 }  // namespace plzgpu

@@ -258,6 +258,50 @@ def test_pinned_host_compress_by_container():
         assert torch.equal(h_out, h_in)
 
 
+def test_pinned_host_decompress_pipeline():
+    # A pinned host image into a pinned host output takes the overlapped path
+    # (image segments up, per-chunk waits in the decode kernel, output
+    # segments down as they complete); tails come from the host walk.  A
+    # corrupt image must fail exactly as the resident path does.
+    import numpy as np
+    import torch
+
+    ctx = plz.context()
+    for S, C, bb, size in ((1, 4096, 16 << 20, (70 << 20) + 3), (2, 2048, 32 << 20, (100 << 20) + 4097),
+                           (4, 1024, 64 << 20, (150 << 20) + 3)):
+        p = P(S, 255, C, 2, bb)
+        data = np.frombuffer(inputs.make("quant", size, 7 * S + size, S), dtype=np.uint8)
+        h_in = torch.from_numpy(data.copy()).pin_memory()
+        dev = plz.compress(h_in.cuda(), p)
+        n_img = dev.numel()
+        h_img = dev.cpu().pin_memory()
+        h_out = torch.zeros(size, dtype=torch.uint8).pin_memory()
+        assert ctx.decompress_ptr(h_img.data_ptr(), n_img, h_out.data_ptr(), size) == size
+        assert torch.equal(h_out, h_in)
+        # corrupt flag bytes in the middle of the image and a truncation
+        for mode in ("flags", "trunc"):
+            bad = h_img.clone()
+            if mode == "flags":
+                bad[n_img // 2: n_img // 2 + 64] ^= 0x5A
+                nb = n_img
+            else:
+                nb = n_img - 1000
+            try:
+                want = plz.decompress_bytes(bad[:nb].cuda()).cpu()
+            except Exception as e:  # noqa: BLE001
+                want = (type(e), str(e))
+            try:
+                got = h_out[:ctx.decompress_ptr(bad.data_ptr(), nb, h_out.data_ptr(), size)]
+            except Exception as e:  # noqa: BLE001
+                got = (type(e), str(e))
+            if isinstance(want, tuple) or isinstance(got, tuple):
+                assert got == want, (mode, got, want)
+            else:
+                assert torch.equal(got, want), mode
+            if mode == "trunc":
+                assert isinstance(want, tuple)
+
+
 def test_device_resident_path_matches_host_path():
     import torch
 
