@@ -222,6 +222,16 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     return v;
 }
 
+// One aligned payload word per lane: the window [base, base + 128) with
+// base = (pay + in) rounded down to 4.  A word is read only if it starts
+// inside the stream (an aligned word holding a stream byte never leaves the
+// allocation).
+__device__ __forceinline__ uint32_t load_window(const uint8_t* pay, uint32_t np, uint32_t in,
+                                                uint32_t lane) {
+    const uintptr_t a = (reinterpret_cast<uintptr_t>(pay + in) & ~uintptr_t(3)) + 4u * lane;
+    return a < reinterpret_cast<uintptr_t>(pay + np) ? *reinterpret_cast<const uint32_t*>(a) : 0u;
+}
+
 // decode_chunk_warp for the common case — the chunk's output fits the warp's
 // shared-memory stage — with chunk-local 32-bit positions and shared-window
 // addresses.  Same token semantics and error order.  Per batch of 32 tokens:
@@ -240,23 +250,39 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
     uint32_t written = 0, in = 0, t = 0;
     const uint32_t below = (1u << lane) - 1u, upto = (2u << lane) - 1u;
     const uint32_t s_bm = static_cast<uint32_t>(__cvta_generic_to_shared(bm));
+    // Each batch's flag byte and a 128-byte payload window (one aligned word
+    // per lane) are loaded one batch ahead, before the previous batch's
+    // waves, so their latency overlaps the copies.  A batch consumes at most
+    // 32 * max(S, 2) <= 128 payload bytes; a token that falls off the window
+    // (S = 4, almost all literals) reads global memory directly.
+    uint32_t fbyte = (lane >> 3) < nf ? flags[lane >> 3] : 0u;
+    uint32_t win = load_window(pay, np, 0, lane);
     while (written < L) {
         const uint32_t tt = t + lane;
         const bool hf = (tt >> 3) < nf;
-        const uint32_t bit = hf ? (uint32_t(flags[tt >> 3]) >> (7u - (tt & 7u))) & 1u : 0u;
+        const uint32_t bit = hf ? (fbyte >> (7u - (tt & 7u))) & 1u : 0u;
         const uint32_t pmask = __ballot_sync(0xffffffffu, bit);
         const uint32_t nptr = __popc(pmask & below);
         const uint32_t pin = in + 2u * nptr + uint32_t(S) * (lane - nptr);
         const uint32_t sz = bit ? 2u : uint32_t(S);
         const bool has = pin + sz <= np;
+        const uint32_t o = pin - in + uint32_t(reinterpret_cast<uintptr_t>(pay + in) & 3u);
+        const uint32_t wa = __shfl_sync(0xffffffffu, win, (o >> 2) & 31u);
+        const uint32_t wb = __shfl_sync(0xffffffffu, win, ((o >> 2) + 1u) & 31u);
+        uint32_t v = __funnelshift_r(wa, wb, 8u * (o & 3u));
         uint32_t len = 0, off = 0, lit = 0;
         if (has) {
-            if (bit) {
-                len = pay[pin];
-                off = pay[pin + 1];
-            } else {
+            if (o + sz > 128u) {
+                v = 0;
 #pragma unroll
-                for (int b = 0; b < S; ++b) lit |= uint32_t(pay[pin + b]) << (8 * b);
+                for (int b = 0; b < (S > 2 ? S : 2); ++b)
+                    if (uint32_t(b) < sz) v |= uint32_t(pay[pin + b]) << (8 * b);
+            }
+            if (bit) {
+                len = v & 0xffu;
+                off = (v >> 8) & 0xffu;
+            } else {
+                lit = S == 4 ? v : v & ((1u << (8 * S)) - 1u);
             }
         }
         const uint32_t adv = bit ? len : 1u;
@@ -286,6 +312,13 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
         if (act && !bit) sts_sym<S>(s_out + pos * S, lit);
         const uint32_t la = first_end - 1;
         const uint32_t span = __shfl_sync(0xffffffffu, incl, la);
+        in = __shfl_sync(0xffffffffu, pin + sz, la);
+        t += first_end;
+        if (written + span < L) {  // the next batch's loads
+            const uint32_t fi = (t + lane) >> 3;
+            fbyte = fi < nf ? flags[fi] : 0u;
+            win = load_window(pay, np, in, lane);
+        }
         if (pmask & (first_end >= 32u ? 0xffffffffu : (1u << first_end) - 1u)) {
             // token table: -off for a pointer, 0 for a literal (its positions
             // then copy onto themselves)
@@ -329,8 +362,6 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
             }
         }
         written += span;
-        in = __shfl_sync(0xffffffffu, pin + sz, la);
-        t += first_end;
     }
     if (in != np) {
         *err_tok = t;
@@ -579,8 +610,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
 // Pipelined host image: waits (lane 0, bounded ~4 s) until the H2D segment
 // holding image byte `b` has landed; all earlier segments land before it.
 // bar.warp.sync in the broadcast orders the other lanes' later loads.
-__device__ __forceinline__ bool wait_image(const DecodeArgs& a, uint64_t b, uint32_t lane) {
-    if (!a.in_ready) return true;
+__device__ __forceinline__ bool wait_image(const DecodePipe& a, uint64_t b, uint32_t lane) {
     uint32_t ok = 1;
     if (lane == 0) {
         const uint32_t* f = a.in_ready + b / a.in_seg;
@@ -597,14 +627,14 @@ __device__ __forceinline__ bool wait_image(const DecodeArgs& a, uint64_t b, uint
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
-template <int S>
+template <int S, bool kPipe>
 __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const ContainerDesc& d,
                                                      uint64_t k, uint8_t* stage, uint32_t lane,
-                                                     uint64_t* err_tok) {
+                                                     uint64_t* err_tok, const DecodePipe& pp) {
     // table entries k, k+1 of both tables: lanes 0-7 payload, 8-15 flags
     const uint8_t* ptab = a.img + d.img_off + 26;
     const uint8_t* ftab = ptab + 4 * (uint64_t(d.num_chunks) + 1);
-    if (!wait_image(a, uint64_t(ftab - a.img) + 4 * k + 7, lane)) {
+    if (kPipe && !wait_image(pp, uint64_t(ftab - a.img) + 4 * k + 7, lane)) {
         *err_tok = 0;
         return TE_OK;  // stalled: the host reports it
     }
@@ -631,7 +661,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
         return TE_OK;
     }
     // the chunk's streams plus the decoder's read-ahead slack
-    if (!wait_image(a, min(d.payload_off + p1 + 127, a.img_len - 1), lane)) {
+    if (kPipe && !wait_image(pp, min(d.payload_off + p1 + 127, a.img_len - 1), lane)) {
         *err_tok = 0;
         return TE_OK;
     }
@@ -685,19 +715,23 @@ __device__ __forceinline__ uint64_t find_container(const ContainerDesc* desc, ui
     return lo;
 }
 
+template <bool kPipe = false>
 __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uint64_t g,
                                                         uint8_t* stage, uint32_t lane,
-                                                        uint64_t* k, uint64_t* tok) {
+                                                        uint64_t* k, uint64_t* tok,
+                                                        const DecodePipe& pp = DecodePipe{}) {
     const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
     *k = g - d.chunk_base;
     switch (d.S) {
-        case 1: return decode_one_chunk<1>(a, d, *k, stage, lane, tok);
-        case 2: return decode_one_chunk<2>(a, d, *k, stage, lane, tok);
-        default: return decode_one_chunk<4>(a, d, *k, stage, lane, tok);
+        case 1: return decode_one_chunk<1, kPipe>(a, d, *k, stage, lane, tok, pp);
+        case 2: return decode_one_chunk<2, kPipe>(a, d, *k, stage, lane, tok, pp);
+        default: return decode_one_chunk<4, kPipe>(a, d, *k, stage, lane, tok, pp);
     }
 }
 
-__global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a) {
+// kPipe: the pipelined host path (per-chunk segment waits, output counts)
+template <bool kPipe>
+__global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = lane_id();
     uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kDecodeWarpSmem;
@@ -708,9 +742,9 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArg
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= total) break;
         uint64_t k, tok;
-        const uint32_t e = decode_global_chunk(a, g, stage, lane, &k, &tok);
+        const uint32_t e = decode_global_chunk<kPipe>(a, g, stage, lane, &k, &tok, pp);
         if (e != TE_OK && lane == 0) atomicMin(a.err_chunk, (unsigned long long)g);
-        if (a.out_done) {
+        if (kPipe) {
             // counted whatever the outcome (the D2H stream must never wait
             // forever); a failed call is re-run on the resident path
             __threadfence_system();
@@ -720,10 +754,10 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArg
                 const uint64_t CS = uint64_t(d.chunk_size) * d.S;
                 const uint64_t o0 = d.out_off + k * CS;
                 const uint64_t o1 = o0 + (k + 1 == d.num_chunks ? uint64_t(d.last_len) * d.S : CS);
-                for (uint64_t sg = o0 / a.out_seg; sg * a.out_seg < o1; ++sg) {
-                    const uint64_t lo = max(o0, sg * a.out_seg);
-                    const uint64_t hi = min(o1, (sg + 1) * a.out_seg);
-                    atomicAdd(a.out_done + sg, uint32_t(hi - lo));
+                for (uint64_t sg = o0 / pp.out_seg; sg * pp.out_seg < o1; ++sg) {
+                    const uint64_t lo = max(o0, sg * pp.out_seg);
+                    const uint64_t hi = min(o1, (sg + 1) * pp.out_seg);
+                    atomicAdd(pp.out_done + sg, uint32_t(hi - lo));
                 }
             }
         }
@@ -789,8 +823,9 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 int decode_ctas_per_sm() {
     int blocks = 0;
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
-    cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel, kDecodeWarps * 32,
+    cudaFuncSetAttribute(plz_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel<false>, kDecodeWarps * 32,
                                                   smem);
     return blocks;
 }
@@ -801,8 +836,16 @@ void launch_parse(const DecodeArgs& a, cudaStream_t st) {
 
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
-    cudaFuncSetAttribute(plz_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    plz_decode_kernel<<<grid, kDecodeWarps * 32, smem, st>>>(a);
+    cudaFuncSetAttribute(plz_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    plz_decode_kernel<false><<<grid, kDecodeWarps * 32, smem, st>>>(a, DecodePipe{});
+}
+
+void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st) {
+    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
+    cudaFuncSetAttribute(plz_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    plz_decode_kernel<true><<<grid, kDecodeWarps * 32, smem, st>>>(a, pp);
 }
 
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
@@ -821,7 +864,8 @@ void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {
 
 void preload_decode_kernels() {
     for (const void* f : {reinterpret_cast<const void*>(plz_parse_kernel),
-                          reinterpret_cast<const void*>(plz_decode_kernel),
+                          reinterpret_cast<const void*>(plz_decode_kernel<false>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<true>),
                           reinterpret_cast<const void*>(plz_chunk_detail_kernel),
                           reinterpret_cast<const void*>(plz_mono_detail_kernel),
                           reinterpret_cast<const void*>(plz_decode_one_kernel)})

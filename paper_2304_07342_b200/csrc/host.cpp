@@ -830,15 +830,16 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     a.err_chunk = &m->err_chunk;
     a.mono_key = &m->mono_key;
     a.work = &m->work[2];
-    a.in_ready = c->ready.as<uint32_t>();
-    a.epoch = c->epoch;
-    a.stalled = &m->stalled;
-    a.in_seg = seg_in;
-    a.out_done = c->done.as<uint32_t>();
-    a.out_seg = seg_out;
+    DecodePipe pp{};
+    pp.in_ready = c->ready.as<uint32_t>();
+    pp.epoch = c->epoch;
+    pp.stalled = &m->stalled;
+    pp.in_seg = seg_in;
+    pp.out_done = c->done.as<uint32_t>();
+    pp.out_seg = seg_out;
     int per_sm = decode_ctas_per_sm();
     if (per_sm < 1) per_sm = 1;
-    launch_decode(a, c->sms * per_sm, st);
+    launch_decode_pipelined(a, pp, c->sms * per_sm, st);
     CK(cudaGetLastError());
     // the image up, segment by segment, after the flags' reset above
     CK(cudaStreamWaitEvent(c->copy_stream, c->asm_ev[0], 0));
@@ -846,14 +847,14 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
         const uint64_t lo = sg * seg_in, hi = std::min(len, lo + seg_in);
         CK(cudaMemcpyAsync(c->img.as<uint8_t>() + lo, img + lo, hi - lo, cudaMemcpyHostToDevice,
                            c->copy_stream));
-        if (write_value(c->copy_stream, reinterpret_cast<unsigned long long>(a.in_ready + sg),
+        if (write_value(c->copy_stream, reinterpret_cast<unsigned long long>(pp.in_ready + sg),
                         c->epoch, 0) != 0)
             return 0;
     }
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
     for (uint64_t sg = 0; sg < nseg_out; ++sg) {
-        if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(a.out_done + sg),
+        if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(pp.out_done + sg),
                        expect[sg], 0) != 0)
             return 0;
         const uint64_t lo = sg * seg_out, hi = std::min(total_out, lo + seg_out);

@@ -249,10 +249,12 @@ struct DecodeArgs {
     // first table-monotonicity violation (global chunk << 1 | flag table),
     // ~0 if none; null: not checked (size-only walks)
     unsigned long long* mono_key;
-    // optional H2D/D2H pipeline of host buffers (plzgpu_decompress): image
-    // byte b may be read once in_ready[b / in_seg] == epoch; each chunk adds
-    // its decoded bytes to out_done[o / out_seg] for every output segment it
-    // covers once they are written (the D2H stream waits on those counts)
+};
+// H2D/D2H pipeline of host buffers (plzgpu_decompress): image byte b may be
+// read once in_ready[b / in_seg] == epoch; each chunk adds its decoded bytes
+// to out_done[o / out_seg] for every output segment it covers once they are
+// written (the D2H stream waits on those counts)
+struct DecodePipe {
     const uint32_t* in_ready;
     uint32_t epoch;
     uint32_t* stalled;
@@ -262,6 +264,7 @@ struct DecodeArgs {
 };
 void launch_parse(const DecodeArgs& a, cudaStream_t st);
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
+void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st);
 // re-decodes chunk *a.err_chunk and reports (TokenErr, chunk within container, token)
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st);
