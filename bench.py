@@ -395,6 +395,18 @@ def run_b200(args):
     e2e_d_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
     e2e_ok = bytes(h_img[:n_img].numpy().tobytes()) == bytes(img[:n_img].cpu().numpy().tobytes())
     e2e_dec_ok = bool(torch.equal(h_out, h_in))
+    # the link's own ceiling: plain pinned copies of the same n bytes
+    link = {}
+    for name, fn in (("h2d_gbs", lambda: d_in.copy_(h_in, non_blocking=True)),
+                     ("d2h_gbs", lambda: h_out.copy_(d_in, non_blocking=True))):
+        with torch.cuda.stream(stream):
+            fn()
+            ev[0].record(stream)
+            for _ in range(3):
+                fn()
+            ev[1].record(stream)
+        torch.cuda.synchronize()
+        link[name] = n * 3 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
 
     if rank != 0:
         if world > 1:
@@ -434,7 +446,9 @@ def run_b200(args):
                 "matches_device_image": e2e_ok,
                 "decompress": {"value": total_in / (e2e_d_ms * 1e-3) / 1e9, "unit": "GB/s",
                                "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n,
-                               "roundtrip_ok": e2e_dec_ok}},
+                               "roundtrip_ok": e2e_dec_ok},
+                "link": {**link, "note": "plain pinned cudaMemcpy of the same bytes: "
+                                         "the PCIe ceiling e2e runs against"}},
         "roofline": {"kernel": "plz_bitmatch_kernel (Kernel I, bitmap pass)", "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_kind": peak_kind,

@@ -731,7 +731,10 @@ uint32_t host_le32(const uint8_t* b) {
 int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, uint8_t* out,
                              uint64_t cap, uint64_t* out_len, cudaStream_t st,
                              plzgpu_error* err) {
-    const uint64_t seg_in = 16ull << 20, seg_out = 32ull << 20;
+    const char* ei = std::getenv("PLZGPU_DSEG_IN_MB");   // A/B: segment sizes
+    const char* eo = std::getenv("PLZGPU_DSEG_OUT_MB");
+    const uint64_t seg_in = uint64_t(ei ? std::max(1, std::atoi(ei)) : 16) << 20;
+    const uint64_t seg_out = uint64_t(eo ? std::max(1, std::atoi(eo)) : 32) << 20;
     StreamWriteValue32Fn write_value = stream_write_value32();
     StreamWaitValue32Fn wait_value = stream_wait_value32();
     if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC")) return 0;
