@@ -737,7 +737,8 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     const uint64_t seg_out = uint64_t(eo ? std::max(1, std::atoi(eo)) : 32) << 20;
     StreamWriteValue32Fn write_value = stream_write_value32();
     StreamWaitValue32Fn wait_value = stream_wait_value32();
-    if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC")) return 0;
+    if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC") || getenv_flag("PLZGPU_NO_PIPE"))
+        return 0;
     // the container walk (format.cpp:112-185 on a well-formed image)
     std::vector<ContainerDesc> descs;
     uint64_t at = 0, total_out = 0, total_chunks = 0;
@@ -1105,6 +1106,7 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
     const bool per_container =
         host_in && nseg > 1 && geo.n_blocks > 1 && cap >= bound && is_pinned_host(out) &&
         geo.cpb % 4 == 0 && geo.cpb % seg_chunks == 0 && !getenv_flag("PLZGPU_NO_PIPE_ASM") &&
+        !getenv_flag("PLZGPU_NO_PIPE") &&
         (cudaHostGetDevicePointer(&mapped, out, 0) == cudaSuccess || (cudaGetLastError(), false));
     const bool direct = (is_device_ptr(out) || per_container) && cap >= bound;
     uint8_t* img = static_cast<uint8_t*>(out);
@@ -1116,7 +1118,9 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
     }
     Meta* m = dmeta(c);
     StreamWriteValue32Fn write_value = stream_write_value32();
-    if (host_in && write_value && nseg > 1) {
+    // PLZGPU_NO_PIPE: no overlapped host paths (profilers serialise the
+    // copies the waiting kernels depend on)
+    if (host_in && write_value && nseg > 1 && !getenv_flag("PLZGPU_NO_PIPE")) {
         // H2D pipeline: Kernel I starts at once and each warp waits for its
         // chunk's segment; segments land on the copy stream, each followed by
         // a stream memory write of its ready flag.

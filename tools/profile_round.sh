@@ -6,7 +6,7 @@ R=${1:-r1}
 mkdir -p gpurun_out
 timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.err
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ -c 400 --csv \
+PLZGPU_NO_PIPE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ -c 400 --csv \
     --log-file gpurun_out/launches_$R.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 # Kernel I: the first bitmap pass (16 rows) of the second compress call
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
