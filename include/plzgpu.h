@@ -146,6 +146,24 @@ int plzgpu_compress_async(plzgpu_ctx* ctx, const plzgpu_params* params, const vo
 int plzgpu_decompress(plzgpu_ctx* ctx, const void* img, uint64_t len, void* out,
                       uint64_t cap, uint64_t* out_len, void* stream, plzgpu_error* err);
 
+/* Decodes the global chunks [chunk_begin, chunk_end) of an image (chunk
+ * index space of the whole container chain, as plzgpu_num_chunks counts it
+ * for the input) — one rank's share of a sharded decompress (SURVEY.md §8e:
+ * "decompress shards the same way ... by chunk range using the tables").
+ * `out` receives decompressed bytes [*out_begin, *out_begin + *out_len):
+ * start(chunk_begin) to start(chunk_end), where start(g) is chunk g's output
+ * offset, start(0) = 0 and start(total) = the decompressed size, so
+ * consecutive ranges partition the output (tails included where their bytes
+ * fall).  *total_chunks reports the image's chunk count (call with an empty
+ * range to learn it).  Every container header is checked (decoder order);
+ * token errors are those of the range's chunks.  Ranges past the end are
+ * clamped.  out = NULL: only the three sizes, nothing decoded.  Replaces nothing in the reference (its decoder is one process);
+ * the per-rank entry point of dist.decompress_sharded. */
+int plzgpu_decompress_range(plzgpu_ctx* ctx, const void* img, uint64_t len, uint64_t chunk_begin,
+                            uint64_t chunk_end, void* out, uint64_t cap, uint64_t* out_begin,
+                            uint64_t* out_len, uint64_t* total_chunks, void* stream,
+                            plzgpu_error* err);
+
 /* Stream-ordered variant: device image and output; the decoded length lands
  * in *d_out_len.  Errors are reported by plzgpu_ctx_finish. */
 int plzgpu_decompress_async(plzgpu_ctx* ctx, const void* d_img, uint64_t len, void* d_out,

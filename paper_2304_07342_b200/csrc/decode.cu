@@ -764,6 +764,38 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArg
     }
 }
 
+// Chunk-range decode (plzgpu_decompress_range): the output bytes of global
+// chunks [cb, ce) are [start(cb), start(ce)) with start(0) = 0, start(total)
+// = total_out and otherwise the chunk's own output offset, so consecutive
+// ranges partition the output (container tails, and containers without
+// chunks, fall into the range that holds their bytes).  One warp: range
+// bounds into res[0..1], the true chunk count into res[2], and every tail
+// byte inside the range copied to out[byte - start(cb)].
+__device__ __forceinline__ uint64_t chunk_start(const DecodeArgs& a, uint64_t g) {
+    const ParseResult* r = a.result;
+    if (g == 0) return 0;
+    if (g >= r->total_chunks) return r->total_out;
+    const ContainerDesc& d = a.desc[find_container(a.desc, r->n_containers, g)];
+    return d.out_off + (g - d.chunk_base) * uint64_t(d.chunk_size) * d.S;
+}
+
+__global__ void plz_range_kernel(DecodeArgs a, uint64_t cb, uint64_t ce, uint8_t* out,
+                                 uint64_t* res) {
+    const uint64_t lo = chunk_start(a, cb), hi = chunk_start(a, ce);
+    const uint64_t nc = out ? a.result->n_containers : 0;
+    for (uint64_t j = threadIdx.x; j < nc; j += blockDim.x) {
+        const ContainerDesc d = a.desc[j];
+        const uint64_t t1 = d.out_off + d.original_len, t0 = t1 - d.tail_len;
+        for (uint64_t t = max(t0, lo); t < min(t1, hi); ++t)
+            out[t - lo] = a.img[d.payload_off + d.payload_len + (t - t0)];
+    }
+    if (threadIdx.x == 0) {
+        res[0] = lo;
+        res[1] = hi;
+        res[2] = a.result->total_chunks;
+    }
+}
+
 // Error details of the lowest failing chunk (re-decoded by one warp).
 __global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* chunk,
                                         uint64_t* token) {
@@ -841,6 +873,11 @@ void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
     plz_decode_kernel<false><<<grid, kDecodeWarps * 32, smem, st>>>(a, DecodePipe{});
 }
 
+void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, uint64_t* res,
+                  cudaStream_t st) {
+    plz_range_kernel<<<1, 32, 0, st>>>(a, cb, ce, out, res);
+}
+
 void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st) {
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
     cudaFuncSetAttribute(plz_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -868,6 +905,7 @@ void preload_decode_kernels() {
                           reinterpret_cast<const void*>(plz_decode_kernel<true>),
                           reinterpret_cast<const void*>(plz_chunk_detail_kernel),
                           reinterpret_cast<const void*>(plz_mono_detail_kernel),
+                          reinterpret_cast<const void*>(plz_range_kernel),
                           reinterpret_cast<const void*>(plz_decode_one_kernel)})
         preload_kernel(f);
 }

@@ -192,6 +192,7 @@ struct Meta {
                         // second/third bitmap pass, [7] wide pass
     uint32_t stalled;  // H2D pipeline: a segment never arrived
     uint32_t pad;
+    uint64_t range[3];  // plzgpu_decompress_range: output range, total chunks
     ParseResult parse;
 };
 
@@ -1266,6 +1267,108 @@ int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, u
         CK(cudaStreamSynchronize(st));
     }
     *out_len = total;
+    return PLZGPU_OK;
+}
+
+int plzgpu_decompress_range(plzgpu_ctx* c, const void* img, uint64_t len, uint64_t chunk_begin,
+                            uint64_t chunk_end, void* out, uint64_t cap, uint64_t* out_begin,
+                            uint64_t* out_len, uint64_t* total_chunks, void* stream,
+                            plzgpu_error* err) {
+    clear_err(err);
+    *out_begin = 0;
+    *out_len = 0;
+    *total_chunks = 0;
+    if (len == 0) return PLZGPU_OK;
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const uint8_t* d_img = static_cast<const uint8_t*>(img);
+    if (!is_device_ptr(img)) {
+        CK(c->img.ensure(len));
+        CK(cudaMemcpyAsync(c->img.p, img, len, cudaMemcpyHostToDevice, st));
+        d_img = c->img.as<uint8_t>();
+    }
+    const bool query = out == nullptr;  // sizes only
+    const bool direct = query || is_device_ptr(out);
+    Meta* m = dmeta(c);
+    // the header walk over the whole image (every container's checks), no
+    // capacity check and no tails: the range kernel places those
+    DecodeArgs a{};
+    Meta h;
+    for (;;) {
+        if (c->desc.cap < 64 * sizeof(ContainerDesc)) CK(c->desc.ensure(64 * sizeof(ContainerDesc)));
+        CK(cudaMemsetAsync(&m->parse, 0, sizeof m->parse, st));
+        CK(cudaMemsetAsync(&m->err_chunk, 0xff, sizeof m->err_chunk + sizeof m->mono_key, st));
+        CK(cudaMemsetAsync(m->work, 0, sizeof m->work, st));
+        a = DecodeArgs{};
+        a.img = d_img;
+        a.img_len = len;
+        a.out = nullptr;
+        a.out_cap = UINT64_MAX;
+        a.desc = c->desc.as<ContainerDesc>();
+        a.desc_cap = c->desc.cap / sizeof(ContainerDesc);
+        a.result = &m->parse;
+        a.err_chunk = &m->err_chunk;
+        a.mono_key = &m->mono_key;
+        a.work = &m->work[2];
+        launch_parse(a, st);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h.parse.err_kind == 17) {
+            CK(c->desc.ensure(c->desc.cap * 4));
+            continue;
+        }
+        break;
+    }
+    if (h.parse.err_kind != 0) return parse_error(h.parse, err);
+    const uint64_t total = h.parse.total_chunks;
+    const uint64_t ce = std::min(chunk_end, total), cb = std::min(chunk_begin, ce);
+    // output range and tails: into the caller's buffer when it is device
+    // memory, else into the staging buffer (copied back below)
+    uint8_t* d_out = static_cast<uint8_t*>(out);
+    if (!direct) {
+        CK(c->out.ensure(cap + 16));
+        d_out = c->out.as<uint8_t>();
+    }
+    launch_range(a, cb, ce, d_out, m->range, st);  // d_out null: bounds only
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h, c->meta.p, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint64_t lo = h.range[0], hi = h.range[1];
+    *total_chunks = total;
+    if (query) {
+        *out_begin = lo;
+        *out_len = hi - lo;
+        return PLZGPU_OK;
+    }
+    if (hi - lo > cap)
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                       "output buffer too small: need %llu bytes", (unsigned long long)(hi - lo));
+    if (ce > cb) {
+        // the decode kernel over [cb, ce): work counter from cb, bound ce,
+        // output addressed relative to the range's first byte
+        const uint32_t w0 = uint32_t(cb);
+        CK(cudaMemcpyAsync(&m->work[2], &w0, 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(&m->parse.total_chunks, &ce, 8, cudaMemcpyHostToDevice, st));
+        a.out = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(d_out) - lo);
+        a.out_cap = hi;
+        int per_sm = decode_ctas_per_sm();
+        if (per_sm < 1) per_sm = 1;
+        launch_decode(a, c->sms * per_sm, st);
+        CK(cudaGetLastError());
+        c->last_launches = 3;
+        c->last_op = OP_DECOMPRESS;
+        c->last_decode = a;
+        bool grow = false;
+        const int rc = finish_decompress(c, st, &grow, err);
+        if (rc) return rc;
+    }
+    if (!direct && hi > lo) {
+        CK(cudaMemcpyAsync(out, d_out, hi - lo, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    *out_begin = lo;
+    *out_len = hi - lo;
     return PLZGPU_OK;
 }
 

@@ -265,6 +265,10 @@ struct DecodePipe {
 void launch_parse(const DecodeArgs& a, cudaStream_t st);
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
 void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st);
+// chunk-range decode: res[0..2] = output range of chunks [cb, ce), total chunks;
+// writes the tails inside the range to out (relative to res[0])
+void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, uint64_t* res,
+                  cudaStream_t st);
 // re-decodes chunk *a.err_chunk and reports (TokenErr, chunk within container, token)
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st);

@@ -124,6 +124,17 @@ class GpuBackend:
     def new_image(self, n: int):
         return self.torch.empty(max(n, 16), dtype=self.torch.uint8, device=self.device)
 
+    def total_chunks(self, img, stream: int = 0) -> int:
+        return self.ctx.decompress_range(img.data_ptr(), img.numel(), 0, 0, 0, 0, stream)[2]
+
+    def decode_range(self, img, rng: Tuple[int, int], stream: int = 0):
+        b, e = rng
+        _, ln, _ = self.ctx.decompress_range(img.data_ptr(), img.numel(), b, e, 0, 0, stream)
+        out = self.torch.empty(max(ln, 16), dtype=self.torch.uint8, device=self.device)
+        begin, ln, _ = self.ctx.decompress_range(img.data_ptr(), img.numel(), b, e,
+                                                 out.data_ptr(), out.numel(), stream)
+        return out[:ln], begin
+
     def headers(self, n_total: int, plan: Plan, tail: bytes, img, stream: int = 0) -> int:
         return self.ctx.shard_headers(self.params, n_total, plan.totals, tail, img.data_ptr(),
                                       img.numel(), stream)
@@ -221,6 +232,31 @@ def compress_sharded(backend, comm, params: plz.Params, n_total: int, d_local,
     if comm.rank == 0:
         backend.headers(n_total, plan, tail_all, img, stream)
     return img, plan.image_len
+
+
+def decompress_sharded(backend, comm, img, gather: bool = True, stream: int = 0):
+    """Sharded decompress of one image that every rank holds:
+    rank r decodes the global chunk range chunk_ranges(total_chunks, world)[r]
+    (``plzgpu_decompress_range``) — no exchange beyond an all-gather of each
+    slice's (offset, length); with `gather`, rank 0 receives every slice at its
+    offset (P2P) into the whole output.  Returns (output on rank 0 else None,
+    this rank's slice, its offset in the output)."""
+    total = backend.total_chunks(img, stream)
+    rng = chunk_ranges(total, comm.world)[comm.rank]
+    local, begin = backend.decode_range(img, rng, stream)
+    if not gather:
+        return None, local, begin
+    n_local = local.numel()
+    sizes = [tuple(v) for v in comm.allgather([begin, n_local])]
+    n_out = max((b + n for b, n in sizes), default=0)
+    out, segs_by_rank = None, None
+    if comm.rank == 0:
+        out = backend.new_image(n_out)
+        if n_local:
+            backend.copy_into(out, begin, local, 0, n_local)
+        segs_by_rank = [[(b, 0, n)] for b, n in sizes]
+    comm.gather_segments(out, local, [(begin, 0, n_local)], segs_by_rank)
+    return (out[:n_out] if out is not None else None), local, begin
 
 
 def simulate_sharded(params: plz.Params, data, world: int, device: int = 0):

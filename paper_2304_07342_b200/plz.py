@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import threading
 from dataclasses import dataclass
-from typing import List, Optional
+from typing import List, Optional, Tuple
 
 from . import _lib as L
 
@@ -200,6 +200,18 @@ class Context:
                                          C.byref(e)), e)
         return int(out_len.value)
 
+    def decompress_range(self, img: int, n: int, chunk_begin: int, chunk_end: int, out: int,
+                         cap: int, stream: int = 0) -> Tuple[int, int, int]:
+        """plzgpu_decompress_range: decodes global chunks [chunk_begin,
+        chunk_end) into `out` (out = 0: sizes only).  Returns (out_begin,
+        out_len, total_chunks)."""
+        b, ln, tot, e = C.c_uint64(), C.c_uint64(), C.c_uint64(), L.Error()
+        _check(L.lib().plzgpu_decompress_range(self.handle, C.c_void_p(img), n, chunk_begin,
+                                               chunk_end, C.c_void_p(out or None), cap,
+                                               C.byref(b), C.byref(ln), C.byref(tot),
+                                               C.c_void_p(stream or None), C.byref(e)), e)
+        return int(b.value), int(ln.value), int(tot.value)
+
     def decompressed_size(self, img: int, n: int, stream: int = 0) -> int:
         out_len, e = C.c_uint64(), L.Error()
         _check(L.lib().plzgpu_decompressed_size(self.handle, C.c_void_p(img), n, C.byref(out_len),
@@ -366,6 +378,23 @@ def decompress_bytes(img, threads: int = 0):
     out = C.create_string_buffer(max(cap, 1))
     ln = ctx.decompress_ptr(ptr, n, C.addressof(out), cap)
     return out.raw[:ln]
+
+
+def decompress_range(img, chunk_begin: int, chunk_end: int):
+    """Decodes the global chunks [chunk_begin, chunk_end) of a CUDA image
+    tensor: returns (output slice tensor, its offset in the decompressed
+    stream, the image's chunk count) — one rank's share of
+    dist.decompress_sharded."""
+    import torch
+
+    ctx = context()
+    t = img.contiguous().view(torch.uint8).reshape(-1)
+    stream = torch.cuda.current_stream(t.device).cuda_stream
+    _, ln, _ = ctx.decompress_range(t.data_ptr(), t.numel(), chunk_begin, chunk_end, 0, 0, stream)
+    out = torch.empty(max(ln, 16), dtype=torch.uint8, device=t.device)
+    b, ln, tot = ctx.decompress_range(t.data_ptr(), t.numel(), chunk_begin, chunk_end,
+                                      out.data_ptr(), out.numel(), stream)
+    return out[:ln], b, tot
 
 
 def decompress_chunk(flags, payload, logical_len: int, params: Params, chunk_index: int = 0) -> bytes:

@@ -35,6 +35,31 @@ class OracleBackend:
             at = fs + ft[n] + pt[n] + image[at + 25]
         self.cpb = params.block_bytes // (params.chunk_size * params.symbol_width)
 
+    # ---- sharded decompress: the range semantics restated over the image's
+    # headers and the oracle's whole-image decode
+    def _starts(self):
+        at, out_off, base, starts = 0, 0, 0, []
+        while at < len(self.img):
+            S, Cs = self.img[at + 5], struct.unpack_from("<I", self.img, at + 9)[0]
+            orig = struct.unpack_from("<Q", self.img, at + 13)[0]
+            n = struct.unpack_from("<I", self.img, at + 21)[0]
+            starts += [out_off + k * Cs * S for k in range(n)]
+            pt = struct.unpack_from("<I", self.img, at + 26 + 4 * n)[0]
+            ft = struct.unpack_from("<I", self.img, at + 26 + 8 * n + 4)[0]
+            at += 26 + 8 * (n + 1) + pt + ft + self.img[at + 25]
+            out_off += orig
+        return starts, out_off
+
+    def total_chunks(self, img, stream=0):
+        return len(self._starts()[0])
+
+    def decode_range(self, img, rng, stream=0):
+        starts, total_out = self._starts()
+        start = lambda g: 0 if g == 0 else (total_out if g >= len(starts) else starts[g])  # noqa: E731
+        lo, hi = start(rng[0]), start(rng[1])
+        full = O.decompress(self.img)
+        return torch.frombuffer(bytearray(full[lo:hi]) or bytearray(1), dtype=torch.uint8)[:hi - lo], lo
+
     def _touched(self, rng):
         b, e = rng
         out = []
@@ -115,6 +140,44 @@ def _worker(rank, world, port, q):
             q.put(results)
     finally:
         dist.destroy_process_group()
+
+
+def _worker_dec(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        results = []
+        for S, W, Cs, I, bb, size in CASES:
+            p = plz.validate(plz.Params(S, W, Cs, I, bb))
+            data = inputs.make("quant", size, 11, S)
+            image = O.compress(data, O.make_params(S, W, Cs, I, bb))
+            be = OracleBackend(p, image)
+            out, local, begin = D.decompress_sharded(be, D.TorchComm("cpu"), None)
+            if rank == 0:
+                results.append(bytes(out.numpy().tobytes()) == data)
+        if rank == 0:
+            q.put(results)
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + 7 * world + os.getpid() % 1000 + (50 if target is _worker_dec else 0)
+    procs = [ctx.Process(target=target, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    return q.get(timeout=5)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_decompress_over_gloo(world):
+    # each rank decodes its chunk range; rank 0 gathers the slices by offset
+    assert _spawn(_worker_dec, world) == [True] * len(CASES)
 
 
 @pytest.mark.parametrize("world", [2, 3])

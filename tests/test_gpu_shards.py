@@ -33,3 +33,74 @@ def test_more_ranks_than_chunks():
     data = inputs.make("runs", 3 * 4096 + 1, 9, 2)
     d = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
     assert bytes(dist.simulate_sharded(p, d, 8).cpu().numpy().tobytes()) == plz.compress(data, p)
+
+
+# ------------------------------------------------------ sharded decompress
+def _ranges_concat(img_t, world):
+    """Every virtual rank's plzgpu_decompress_range slice, checked to tile the
+    output contiguously, concatenated."""
+    _, _, total = plz.decompress_range(img_t, 0, 0)
+    parts, at = [], 0
+    for b, e in dist.chunk_ranges(total, world):
+        out, begin, tot = plz.decompress_range(img_t, b, e)
+        assert tot == total and begin == at
+        at += out.numel()
+        parts.append(bytes(out.cpu().numpy().tobytes()))
+    return b"".join(parts)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("S,W,C,I,bb", [(2, 255, 2048, 2, 2048 * 2 * 5), (1, 128, 4096, 1, 4096 * 3),
+                                        (4, 255, 1024, 4, 1024 * 4 * 2)])
+def test_sharded_decompress_ranges_tile_the_output(world, S, W, C, I, bb):
+    # chunk ranges cut through containers; tails land in the range holding them
+    import torch
+
+    p = plz.validate(plz.Params(S, W, C, I, bb))
+    data = inputs.make("quant", 23 * C * S + 3 * S + (S - 1), 200 + world, S)
+    img = torch.frombuffer(bytearray(plz.compress(data, p)), dtype=torch.uint8).cuda()
+    assert _ranges_concat(img, world) == data
+
+
+def test_sharded_decompress_of_concatenated_images():
+    # containers with tails and containers without chunks (inputs shorter
+    # than one symbol) between them: every byte belongs to exactly one range
+    import torch
+
+    parts = [inputs.make("alpha", n, n, 4) for n in (4099, 3, 12345, 2, 0, 70001)]
+    imgs = [plz.compress(d, plz.validate(plz.Params(4, 255, 1024, 2, 1024 * 4 * 3))) for d in parts]
+    img = torch.frombuffer(bytearray(b"".join(imgs)), dtype=torch.uint8).cuda()
+    for world in (1, 2, 3, 7, 40):
+        assert _ranges_concat(img, world) == b"".join(parts)
+
+
+def test_sharded_decompress_errors():
+    # a corrupt chunk fails the range holding it (same error as the whole
+    # decode) and no other; a header error fails every range
+    import torch
+
+    p = plz.validate(plz.Params(2, 255, 2048, 1))
+    data = inputs.make("quant", 40 * 4096, 5, 2)
+    good = bytearray(plz.compress(data, p))
+    n = int.from_bytes(good[21:25], "little")
+    flags0 = 26 + 8 * (n + 1)
+    k = 30  # corrupt chunk 30's first flag byte region: set every flag bit
+    fk = int.from_bytes(good[26 + 4 * (n + 1) + 4 * k:26 + 4 * (n + 1) + 4 * k + 4], "little")
+    bad = bytearray(good)
+    bad[flags0 + fk:flags0 + fk + 4] = b"\xff\xff\xff\xff"
+    t = torch.frombuffer(bad, dtype=torch.uint8).cuda()
+    with pytest.raises(plz.CorruptionError) as whole:
+        plz.decompress_bytes(t)
+    with pytest.raises(plz.CorruptionError) as part:
+        plz.decompress_range(t, 20, 40)
+    assert str(part.value) == str(whole.value)
+    out, begin, _ = plz.decompress_range(t, 0, 20)
+    assert bytes(out.cpu().numpy().tobytes()) == data[:begin + out.numel()]
+    hdr = bytearray(good)
+    hdr[4] = 2  # version
+    th = torch.frombuffer(hdr, dtype=torch.uint8).cuda()
+    with pytest.raises(plz.Error) as whole:
+        plz.decompress_bytes(th)
+    with pytest.raises(plz.Error) as part:
+        plz.decompress_range(th, 0, 1)
+    assert type(part.value) is type(whole.value) and str(part.value) == str(whole.value)
