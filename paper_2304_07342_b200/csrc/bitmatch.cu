@@ -425,9 +425,20 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
                 tb += 32u;
             }
             if (p & Im1) {  // forced literals up to the next aligned position
-                const int q = min((p + Im1) & ~Im1, n);
-                literals(p, q);
-                p = q;
+                if ((p & Im1) == Im1 && p < n) {  // exactly one (always, for I = 2)
+                    if (lane == slot) tokv = uint32_t(p);
+                    ++p;
+                    if (++slot == 32u) {
+                        flush_tokens<S, (MAXS + 31) / 32>(tokv, 32u, tb, pl, nptr, tab, s_ids, pay,
+                                                          fl32, lane, a.hist);
+                        slot = 0;
+                        tb += 32u;
+                    }
+                } else {
+                    const int q = min((p + Im1) & ~Im1, n);
+                    literals(p, q);
+                    p = q;
+                }
             }
         }
         if (slot) flush_tokens<S, (MAXS + 31) / 32>(tokv, slot, tb, pl, nptr, tab, s_ids, pay, fl32, lane, a.hist);
