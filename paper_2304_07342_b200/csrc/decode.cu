@@ -336,28 +336,34 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
             const uint32_t s_w = s_out + written * S;
             const uint32_t s_tb = s_tab - 4u;  // index before + popc - 1
             uint32_t before = 0;  // batch tokens starting before the wave
+            uint32_t a_bm = s_bm;                       // start-bitmap word of the wave
+            uint32_t a_q = s_w + lane * uint32_t(S);    // this lane's output slot
+            int wb = 0;                                 // the wave's first position
 #pragma unroll 1
             for (uint32_t w = 0; w < nw; ++w) {
-                const uint32_t starts = lds32(s_bm + 4u * w);
-                const int q = int(w << 5) + int(lane);
+                const uint32_t starts = lds32(a_bm);
                 const int tv = int(lds32(s_tb + 4u * (before + __popc(starts & upto))));
                 // batch-relative source; negative = an earlier batch (final)
-                int src = q + tv;
-                if (__any_sync(0xffffffffu, tv != 0 && src >= int(w << 5))) {
+                int src = wb + int(lane) + tv;
+                // a source inside the wave: 0 < off <= lane
+                if (__any_sync(0xffffffffu, uint32_t(-tv - 1) < lane)) {
                     // sources inside the wave: pointer jumping over the lanes —
                     // a lane whose source is lane r's position takes lane r's
                     // source (a literal lane's source is itself), until every
                     // source is final (a literal or an earlier wave)
                     bool more;
                     do {
-                        const bool in = src >= int(w << 5);
+                        const bool in = src >= wb;
                         const int s2 = __shfl_sync(0xffffffffu, src, uint32_t(src) & 31u);
                         more = in && s2 != src;
                         src = in ? s2 : src;
                     } while (__any_sync(0xffffffffu, more));
                 }
-                sts_sym<S>(s_w + uint32_t(q) * S, lds_sym<S>(uint32_t(int(s_w) + src * S)));
+                sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (src - wb - int(lane)) * S)));
                 before += __popc(starts);
+                a_bm += 4u;
+                a_q += 32u * S;
+                wb += 32;
                 __syncwarp();
             }
         }
