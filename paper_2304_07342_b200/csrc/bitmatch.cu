@@ -117,7 +117,7 @@ __device__ __forceinline__ bool stage_chunk(const EncodeArgs& a, uint64_t ck, in
 // flag word is the ballot of pointer lanes, bit-reversed within each byte
 // (MSB-first, encoder.cpp:33).
 template <int S, int NT>
-__device__ __forceinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32_t t0,
+__device__ __noinline__ void flush_tokens(uint32_t tokv, uint32_t cnt, uint32_t t0,
                                              uint32_t& pl, uint32_t& nptr, const uint32_t (&tab)[NT],
                                              uint32_t s_ids,
                                              uint8_t* pay, uint32_t* fl32, uint32_t lane,
