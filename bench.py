@@ -358,10 +358,51 @@ def run_b200(args):
         s_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
         shard = {"ms_per_step": s_ms, "image_bytes": img_len_s, "input_bytes": n_total,
                  "ratio": n_total / img_len_s, "chunk_range": [cb, ce]}
+        back = None
         if rank == 0:  # the gathered stream decodes to the union of the shards
             back = plz.decompress_bytes(img_s[:img_len_s])
             shard["roundtrip_ok"] = bool(back.numel() == n_total)
         del shard_in
+
+        # sharded decompress of that stream (every rank holds the image, rank
+        # r decodes chunk range r: dist.decompress_sharded, no gather timed)
+        cdev = "cpu" if gloo else dev
+        ln_t = torch.tensor([img_len_s if rank == 0 else 0], dtype=torch.int64, device=cdev)
+        dist.broadcast(ln_t, 0)
+        L_img = int(ln_t.item())
+        if rank == 0:
+            img_full = img_s[:L_img].contiguous()
+        else:
+            img_full = torch.empty(L_img, dtype=torch.uint8, device=dev)
+        if gloo:
+            buf = img_full.cpu()
+            dist.broadcast(buf, 0)
+            img_full = buf.to(dev)
+        else:
+            dist.broadcast(img_full, 0)
+
+        def dec_shard_step(gather=False):
+            with torch.cuda.stream(stream):
+                return D.decompress_sharded(backend, comm, img_full, gather, sh)
+
+        for _ in range(args.warmup):
+            dec_shard_step()
+        barrier()
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            dec_shard_step()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        sd_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
+        whole, _, _ = dec_shard_step(True)
+        shard["decompress"] = {"value": n_total / (sd_ms * 1e-3) / 1e9, "unit": "GB/s",
+                               "ms_per_step": sd_ms,
+                               "note": "dist.decompress_sharded: rank r decodes chunk range r "
+                                       "of the one image (plzgpu_decompress_range), no gather"}
+        if rank == 0:
+            shard["decompress"]["roundtrip_ok"] = bool(torch.equal(whole.to(back.device), back))
+        del img_full, whole
 
     # ---- end to end through the public call with host buffers
     h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
