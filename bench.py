@@ -457,6 +457,8 @@ def run_b200(args):
 
     total_in = n * world
     peak, peak_kind = load_peaks()
+    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+    int_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * sm_mhz * 1e6
     prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {[1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]}, 16>")
     enc_bytes = n + n_img  # input read + staged tokens written (~ image)
     achieved = enc_bytes / (enc_ms * 1e-3) / 1e9
@@ -505,7 +507,13 @@ def run_b200(args):
                      # matcher's work, which Kernel I's bitmaps replace with
                      # W/32 word operations per step
                      "match_pairs": {"pairs_per_launch": match_pairs(n, w),
-                                     "pairs_per_s": match_pairs(n, w) / (enc_ms * 1e-3)}},
+                                     "pairs_per_s": match_pairs(n, w) / (enc_ms * 1e-3),
+                                     # SURVEY.md §8d's int_fraction: pairs/s over the
+                                     # int32 lane-op peak (148 SMs x 128 lanes x clock);
+                                     # > 1 would be possible — a bitmap word op covers
+                                     # 32 pairs
+                                     "int_peak_ops_per_s": int_peak,
+                                     "int_fraction": match_pairs(n, w) / (enc_ms * 1e-3) / int_peak}},
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
         "gpu_launches": (launches if world == 1 else 4) * args.steps,
         "clocks": clk.summary(),
