@@ -220,6 +220,12 @@ struct plzgpu_ctx {
     cudaStream_t side_stream = nullptr;  // Kernel I: the 64-row pass beside the 32-row one
     cudaEvent_t side_ev[2] = {nullptr, nullptr};
     cudaEvent_t asm_ev[2] = {nullptr, nullptr};
+    // pipelined compress into pinned host memory: per container, its scan
+    // and its assembly done; the image goes down on d2h_stream, the
+    // container sizes that place it come back on size_stream
+    std::vector<cudaEvent_t> cont_ev;
+    cudaStream_t d2h_stream = nullptr, size_stream = nullptr;
+    uint64_t* host_scratch = nullptr;  // pinned, 4 words
     DevBuf ready, done;
     uint32_t epoch = 0;
     const uint32_t* pipe_ready = nullptr;  // set while enqueueing a pipelined encode
@@ -506,6 +512,11 @@ int enqueue_compress_by_container(plzgpu_ctx* c, const plzgpu_params& p, const u
     for (cudaEvent_t& ev : c->asm_ev)
         if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     Meta* m = dmeta(c);
+    while (c->cont_ev.size() < 2 * g.n_blocks) {
+        cudaEvent_t ev;
+        CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->cont_ev.push_back(ev);
+    }
     int launches = 0;
     for (uint64_t j = 0; j < g.n_blocks; ++j) {
         const uint64_t g0 = j * g.cpb, g1 = std::min(g.n_chunks, g0 + g.cpb);
@@ -514,6 +525,7 @@ int enqueue_compress_by_container(plzgpu_ctx* c, const plzgpu_params& p, const u
         int rc = enqueue_encode_scan(c, p, d_in, g.n_chunks, g.last_len, st, err, &launches, true,
                                      g0, g1, false);
         if (rc) return rc;
+        CK(cudaEventRecord(c->cont_ev[2 * j], st));
         CK(cudaEventRecord(c->asm_ev[0], st));
         CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
         AssembleArgs a{};
@@ -540,6 +552,7 @@ int enqueue_compress_by_container(plzgpu_ctx* c, const plzgpu_params& p, const u
         a.j_hi = j + 1;
         launch_assemble(a, c->asm_stream);
         launch_headers(a, c->asm_stream);
+        CK(cudaEventRecord(c->cont_ev[2 * j + 1], c->asm_stream));
         launches += 2;
     }
     CK(cudaEventRecord(c->asm_ev[1], c->asm_stream));
@@ -842,10 +855,6 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     pp.in_seg = seg_in;
     pp.out_done = c->done.as<uint32_t>();
     pp.out_seg = seg_out;
-    int per_sm = decode_ctas_per_sm();
-    if (per_sm < 1) per_sm = 1;
-    launch_decode_pipelined(a, pp, c->sms * per_sm, st);
-    CK(cudaGetLastError());
     // the image up, segment by segment, after the flags' reset above
     CK(cudaStreamWaitEvent(c->copy_stream, c->asm_ev[0], 0));
     for (uint64_t sg = 0; sg < nseg_in; ++sg) {
@@ -856,6 +865,10 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
                         c->epoch, 0) != 0)
             return 0;
     }
+    int per_sm = decode_ctas_per_sm();
+    if (per_sm < 1) per_sm = 1;
+    launch_decode_pipelined(a, pp, c->sms * per_sm, st);
+    CK(cudaGetLastError());
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
     for (uint64_t sg = 0; sg < nseg_out; ++sg) {
@@ -1066,6 +1079,14 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t& ev : c->asm_ev)
         if (ev) cudaEventDestroy(ev);
+    for (cudaStream_t sx : {c->d2h_stream, c->size_stream})
+        if (sx) {
+            cudaStreamSynchronize(sx);
+            cudaStreamDestroy(sx);
+        }
+    for (cudaEvent_t ev : c->cont_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (c->host_scratch) cudaFreeHost(c->host_scratch);
     if (c->copy_stream) {
         cudaStreamSynchronize(c->copy_stream);
         cudaStreamDestroy(c->copy_stream);
@@ -1095,8 +1116,17 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
     const bool host_in = !is_device_ptr(in);
     const uint64_t bound = plzgpu_compress_bound(n, params);
     const Geometry geo = geometry(n, *params);
-    const char* seg_env = std::getenv("PLZGPU_SEG_MB");  // A/B: H2D segment size
-    const uint64_t seg_bytes_target = uint64_t(seg_env ? std::max(1, std::atoi(seg_env)) : 32) << 20;
+    // H2D pipeline geometry (env overrides for A/B): ready flags every
+    // PLZGPU_SEG_MB, copies of PLZGPU_COPY_MB except over the input's last
+    // PLZGPU_TAIL_MB, sent flag segment by flag segment so the matching
+    // that can only start after the last byte lands is short
+    auto env_mb = [](const char* name, int dflt) {
+        const char* v = std::getenv(name);
+        return uint64_t(v ? std::max(0, std::atoi(v)) : dflt) << 20;
+    };
+    const uint64_t seg_bytes_target = std::max<uint64_t>(env_mb("PLZGPU_SEG_MB", 32), 1);
+    const uint64_t copy_bytes = env_mb("PLZGPU_COPY_MB", 32);
+    const uint64_t tail_bytes = env_mb("PLZGPU_TAIL_MB", 0);
     const uint64_t chunk_bytes = uint64_t(params->chunk_size) * params->symbol_width;
     const uint64_t seg_chunks = std::max<uint64_t>(1, seg_bytes_target / chunk_bytes);
     const uint64_t nseg = (geo.n_chunks + seg_chunks - 1) / seg_chunks;
@@ -1110,10 +1140,13 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
         !getenv_flag("PLZGPU_NO_PIPE") &&
         (cudaHostGetDevicePointer(&mapped, out, 0) == cudaSuccess || (cudaGetLastError(), false));
     const bool direct = (is_device_ptr(out) || per_container) && cap >= bound;
+    // per container: Kernel III into HBM and each finished container down on
+    // the copy engine (default), or Kernel III writing the mapped host image
+    const bool asm_mapped = getenv_flag("PLZGPU_ASM_MAPPED");
     uint8_t* img = static_cast<uint8_t*>(out);
-    if (per_container) {
+    if (per_container && asm_mapped) {
         img = static_cast<uint8_t*>(mapped);
-    } else if (!direct) {
+    } else if (per_container || !direct) {
         CK(c->img.ensure(bound));
         img = c->img.as<uint8_t>();
     }
@@ -1135,6 +1168,24 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
             CK(cudaStreamSynchronize(st));
             ++c->epoch;
         }
+        // the copies first: the H2D stream starts before the launches below
+        // are enqueued (each warp of Kernel I waits for its own segment)
+        const uint64_t seg_bytes = seg_chunks * chunk_bytes;
+        const uint64_t per_copy = std::max<uint64_t>(1, copy_bytes / seg_bytes);
+        const uint64_t tail_from = n > tail_bytes ? n - tail_bytes : 0;
+        for (uint64_t sgi = 0; sgi < nseg;) {
+            const uint64_t lo = sgi * seg_bytes;
+            const uint64_t s_end = lo >= tail_from ? sgi + 1 : std::min(nseg, sgi + per_copy);
+            const uint64_t hi = s_end == nseg ? n : std::min(n, s_end * seg_bytes);
+            CK(cudaMemcpyAsync(c->in.as<uint8_t>() + lo, static_cast<const uint8_t*>(in) + lo,
+                               hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
+            for (; sgi < s_end; ++sgi)
+                if (write_value(c->copy_stream,
+                                reinterpret_cast<unsigned long long>(c->ready.as<uint32_t>() + sgi),
+                                c->epoch, 0) != 0)
+                    return set_err(err, PLZGPU_CUDA, 0, kNoIndex, kNoIndex,
+                                   "cuStreamWriteValue32 failed");
+        }
         c->pipe_ready = c->ready.as<uint32_t>();
         c->pipe_seg_chunks = uint32_t(seg_chunks);
         if (per_container) {
@@ -1144,16 +1195,34 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
         }
         c->pipe_ready = nullptr;
         if (rc) return rc;
-        for (uint64_t sgi = 0; sgi < nseg; ++sgi) {
-            const uint64_t lo = sgi * seg_chunks * chunk_bytes;
-            const uint64_t hi = sgi + 1 == nseg ? n : std::min(n, (sgi + 1) * seg_chunks * chunk_bytes);
-            CK(cudaMemcpyAsync(c->in.as<uint8_t>() + lo, static_cast<const uint8_t*>(in) + lo,
-                               hi - lo, cudaMemcpyHostToDevice, c->copy_stream));
-            if (write_value(c->copy_stream,
-                            reinterpret_cast<unsigned long long>(c->ready.as<uint32_t>() + sgi),
-                            c->epoch, 0) != 0)
-                return set_err(err, PLZGPU_CUDA, 0, kNoIndex, kNoIndex,
-                               "cuStreamWriteValue32 failed");
+        if (per_container && !asm_mapped) {
+            // each container's image range is known once its scan is done
+            // (global stream prefixes P64 / F64 at its first and last chunk):
+            // read the four words, then send the range down after assembly
+            for (cudaStream_t* sx : {&c->d2h_stream, &c->size_stream})
+                if (!*sx) CK(cudaStreamCreateWithFlags(sx, cudaStreamNonBlocking));
+            if (!c->host_scratch)
+                CK(cudaMallocHost(reinterpret_cast<void**>(&c->host_scratch), 4 * sizeof(uint64_t)));
+            uint64_t off = 0;
+            for (uint64_t j = 0; j < geo.n_blocks; ++j) {
+                const uint64_t g0 = j * geo.cpb, g1 = std::min(geo.n_chunks, g0 + geo.cpb);
+                CK(cudaStreamWaitEvent(c->size_stream, c->cont_ev[2 * j], 0));
+                const uint64_t* src[4] = {c->p64.as<uint64_t>() + g0, c->p64.as<uint64_t>() + g1,
+                                          c->f64.as<uint64_t>() + g0, c->f64.as<uint64_t>() + g1};
+                for (int k = 0; k < 4; ++k)
+                    CK(cudaMemcpyAsync(c->host_scratch + k, src[k], 8, cudaMemcpyDeviceToHost,
+                                       c->size_stream));
+                CK(cudaStreamSynchronize(c->size_stream));
+                const uint64_t* v = c->host_scratch;
+                const uint64_t tail = j + 1 == geo.n_blocks ? n % uint64_t(params->symbol_width) : 0;
+                const uint64_t size = 26 + 8 * (g1 - g0 + 1) + (v[3] - v[2]) + (v[1] - v[0]) + tail;
+                if (off + size > cap) break;  // an offset overflow: reported below
+                CK(cudaStreamWaitEvent(c->d2h_stream, c->cont_ev[2 * j + 1], 0));
+                CK(cudaMemcpyAsync(static_cast<uint8_t*>(out) + off, img + off, size,
+                                   cudaMemcpyDeviceToHost, c->d2h_stream));
+                off += size;
+            }
+            CK(cudaStreamSynchronize(c->d2h_stream));
         }
     } else {
         if (host_in) {
