@@ -487,21 +487,16 @@ int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta) {
     int blocks = 0;
     const size_t smem = bm_warp_smem(C, S, W, maxsyms) * warps_per_cta;
     const void* fn = bitmatch_fn(S, W, maxsyms);
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-        cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
+    if (!smem_fits(fn, smem)) return 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, warps_per_cta * 32, smem);
     return blocks;
 }
 
-void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = bm_warp_smem(a.C, S, a.W, maxsyms) * a.warps_per_cta;
     const void* fn = bitmatch_fn(S, a.W, maxsyms);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     void* args[] = {const_cast<EncodeArgs*>(&a)};
-    cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
 void preload_bitmatch_kernels() {

@@ -861,8 +861,6 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 int decode_ctas_per_sm() {
     int blocks = 0;
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
-    cudaFuncSetAttribute(plz_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel<false>, kDecodeWarps * 32,
                                                   smem);
     return blocks;
@@ -874,8 +872,6 @@ void launch_parse(const DecodeArgs& a, cudaStream_t st) {
 
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
-    cudaFuncSetAttribute(plz_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
     plz_decode_kernel<false><<<grid, kDecodeWarps * 32, smem, st>>>(a, DecodePipe{});
 }
 
@@ -886,8 +882,6 @@ void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, u
 
 void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st) {
     const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
-    cudaFuncSetAttribute(plz_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
     plz_decode_kernel<true><<<grid, kDecodeWarps * 32, smem, st>>>(a, pp);
 }
 

@@ -529,18 +529,12 @@ void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, 
     const dim3 block(a.warps_per_cta * 32);
     switch (S) {
         case 1:
-            cudaFuncSetAttribute(plz_match_table_kernel<1>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             plz_match_table_kernel<1><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
             break;
         case 2:
-            cudaFuncSetAttribute(plz_match_table_kernel<2>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             plz_match_table_kernel<2><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
             break;
         default:
-            cudaFuncSetAttribute(plz_match_table_kernel<4>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
             plz_match_table_kernel<4><<<grid, block, smem, st>>>(a, len_out, off_out, raw_hist);
             break;
     }
@@ -556,17 +550,16 @@ int encode_ctas_per_sm(int S, int C, int warps_per_cta) {
     int blocks = 0;
     const size_t smem = encode_warp_smem(C, S) * warps_per_cta;
     const void* fn = encode_kernel_for(S);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (!smem_fits(fn, smem)) return 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, warps_per_cta * 32, smem);
     return blocks;
 }
 
-void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st) {
     const size_t smem = encode_warp_smem(a.C, S) * a.warps_per_cta;
     const void* fn = encode_kernel_for(S);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     void* args[] = {const_cast<EncodeArgs*>(&a)};
-    cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
+    return cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
 void preload_encode_kernels() {

@@ -360,6 +360,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     encode_shape(c, p, kBmMaxSyms, &wpc1, &per_sm1);
     const bool classify = side_passes && Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
     e.classify = classify ? 1 : 0;
+    cudaError_t launch_err = cudaSuccess;  // first failed bitmap-pass launch
     auto bitmap_pass = [&](int maxsyms, int pass, const uint32_t* src, const uint32_t* src_n,
                            uint32_t* ovf, uint32_t* ovf_n, cudaStream_t s) -> bool {
         int wpc = 1, per_sm = 0;
@@ -382,7 +383,8 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         // container's Kernel III on the assembly stream
         const int resident = side_passes ? per_sm : std::max(1, per_sm - 1);
         const uint64_t ctas = std::min<uint64_t>(uint64_t(c->sms) * resident, (Gr + wpc - 1) / wpc);
-        launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), s);
+        const cudaError_t le = launch_bitmatch(p.symbol_width, maxsyms, b, int(ctas), s);
+        if (le != cudaSuccess && launch_err == cudaSuccess) launch_err = le;
         ++*launches;
         return true;
     };
@@ -424,11 +426,13 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         f.src_count = wide_n;
         if (wide_src) f.ready = nullptr;
         f.warps_per_cta = wpc;
-        launch_encode(p.symbol_width, f,
-                      int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1), (Gr + wpc - 1) / wpc)),
-                      st);
+        CK(launch_encode(p.symbol_width, f,
+                         int(std::min<uint64_t>(uint64_t(c->sms) * std::max(per_sm, 1),
+                                                (Gr + wpc - 1) / wpc)),
+                         st));
         ++*launches;
     }
+    CK(launch_err);
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
     ScanArgs sa{};
@@ -745,10 +749,18 @@ uint32_t host_le32(const uint8_t* b) {
 int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, uint8_t* out,
                              uint64_t cap, uint64_t* out_len, cudaStream_t st,
                              plzgpu_error* err) {
-    const char* ei = std::getenv("PLZGPU_DSEG_IN_MB");   // A/B: segment sizes
-    const char* eo = std::getenv("PLZGPU_DSEG_OUT_MB");
-    const uint64_t seg_in = uint64_t(ei ? std::max(1, std::atoi(ei)) : 16) << 20;
-    const uint64_t seg_out = uint64_t(eo ? std::max(1, std::atoi(eo)) : 32) << 20;
+    // Ready flags every seg_in bytes of image, output counters every seg_out
+    // bytes; the first kLead transfers each way move one segment, later ones
+    // kGroup segments at a time.  Env overrides for A/B (2/4 MiB segments
+    // with 4 single and then 8-segment transfers measured no faster).
+    auto env_int = [](const char* name, int dflt) {
+        const char* v = std::getenv(name);
+        return v ? std::max(1, std::atoi(v)) : dflt;
+    };
+    const uint64_t seg_in = uint64_t(env_int("PLZGPU_DSEG_IN_MB", 16)) << 20;
+    const uint64_t seg_out = uint64_t(env_int("PLZGPU_DSEG_OUT_MB", 32)) << 20;
+    const uint64_t kLead = uint64_t(env_int("PLZGPU_DSEG_LEAD", 1));
+    const uint64_t kGroup = uint64_t(env_int("PLZGPU_DSEG_GROUP", 1));
     StreamWriteValue32Fn write_value = stream_write_value32();
     StreamWaitValue32Fn wait_value = stream_wait_value32();
     if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC") || getenv_flag("PLZGPU_NO_PIPE"))
@@ -857,13 +869,15 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     pp.out_seg = seg_out;
     // the image up, segment by segment, after the flags' reset above
     CK(cudaStreamWaitEvent(c->copy_stream, c->asm_ev[0], 0));
-    for (uint64_t sg = 0; sg < nseg_in; ++sg) {
-        const uint64_t lo = sg * seg_in, hi = std::min(len, lo + seg_in);
+    for (uint64_t sg = 0; sg < nseg_in;) {
+        const uint64_t s_end = std::min(nseg_in, sg + (sg < kLead ? 1 : kGroup));
+        const uint64_t lo = sg * seg_in, hi = std::min(len, s_end * seg_in);
         CK(cudaMemcpyAsync(c->img.as<uint8_t>() + lo, img + lo, hi - lo, cudaMemcpyHostToDevice,
                            c->copy_stream));
-        if (write_value(c->copy_stream, reinterpret_cast<unsigned long long>(pp.in_ready + sg),
-                        c->epoch, 0) != 0)
-            return 0;
+        for (; sg < s_end; ++sg)
+            if (write_value(c->copy_stream, reinterpret_cast<unsigned long long>(pp.in_ready + sg),
+                            c->epoch, 0) != 0)
+                return 0;
     }
     int per_sm = decode_ctas_per_sm();
     if (per_sm < 1) per_sm = 1;
@@ -871,11 +885,13 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     CK(cudaGetLastError());
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
-    for (uint64_t sg = 0; sg < nseg_out; ++sg) {
-        if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(pp.out_done + sg),
-                       expect[sg], 0) != 0)
-            return 0;
-        const uint64_t lo = sg * seg_out, hi = std::min(total_out, lo + seg_out);
+    for (uint64_t sg = 0; sg < nseg_out;) {
+        const uint64_t s_end = std::min(nseg_out, sg + (sg < kLead ? 1 : kGroup));
+        const uint64_t lo = sg * seg_out, hi = std::min(total_out, s_end * seg_out);
+        for (; sg < s_end; ++sg)
+            if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(pp.out_done + sg),
+                           expect[sg], 0) != 0)
+                return 0;
         CK(cudaMemcpyAsync(out + lo, a.out + lo, hi - lo, cudaMemcpyDeviceToHost, c->asm_stream));
     }
     CK(cudaEventRecord(c->asm_ev[1], c->asm_stream));

@@ -113,10 +113,10 @@ struct EncodeArgs {
     int classify;                // first pass: sort its overflow by alphabet size (else list 0)
 };
 // the wide-cell kernel (any alphabet)
-void launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st);
 // the bitmap kernel (bitmatch.cu): chunks with <= maxsyms distinct symbols
 // (maxsyms = kBmMaxSyms, kBmMaxSymsMid or kBmMaxSymsWide)
-void launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st);
 int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
 void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
@@ -279,9 +279,31 @@ int decode_ctas_per_sm();
 // behind a kernel that spins on H2D segments the host has not enqueued yet
 // would stall the pipeline.  Each file's kernels are loaded up front instead
 // (cudaFuncGetAttributes forces the load).
+// The same pass raises each kernel's dynamic shared-memory limit to the
+// device's opt-in maximum once; launches never set it again (a limit set per
+// launch races between host threads: one thread's occupancy probe could
+// lower it between another's set and launch, failing that launch).
 inline void preload_kernel(const void* f) {
     cudaFuncAttributes at;
-    if (cudaFuncGetAttributes(&at, f) != cudaSuccess) (void)cudaGetLastError();
+    if (cudaFuncGetAttributes(&at, f) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return;
+    }
+    int dev = 0, optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - int(at.sharedSizeBytes)) != cudaSuccess)
+        (void)cudaGetLastError();
+}
+// whether `smem` dynamic bytes fit the kernel's (preloaded) limit
+inline bool smem_fits(const void* f, size_t smem) {
+    cudaFuncAttributes at;
+    if (cudaFuncGetAttributes(&at, f) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    return smem <= size_t(at.maxDynamicSharedSizeBytes);
 }
 void preload_assemble_kernels();
 void preload_scan_kernels();

@@ -199,16 +199,22 @@ def test_concurrent_host_threads_give_identical_images():
     got = [None] * len(inputs_)
     back = [None] * len(inputs_)
 
+    errors = [None] * len(inputs_)
+
     def work(i):
-        for _ in range(3):
-            got[i] = plz.compress(inputs_[i], p)
-            back[i] = plz.decompress_bytes(got[i])
+        try:
+            for _ in range(3):
+                got[i] = plz.compress(inputs_[i], p)
+                back[i] = plz.decompress_bytes(got[i])
+        except Exception as e:  # noqa: BLE001 — reported below with the thread's index
+            errors[i] = repr(e)
 
     ts = [threading.Thread(target=work, args=(i,)) for i in range(len(inputs_))]
     for t in ts:
         t.start()
     for t in ts:
         t.join()
+    assert errors == [None] * len(inputs_), errors
     assert got == want
     assert back == inputs_
 
