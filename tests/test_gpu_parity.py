@@ -448,3 +448,35 @@ def test_invalid_params_raise_validation_error(field):
     setattr(raw, field, bad)
     with pytest.raises(plz.ValidationError):
         plz.compress(b"abc", raw)
+
+
+def test_random_grid_fuzz_against_the_reference():
+    # random (S, W, C, I, block_bytes, size, input kind) over the whole
+    # parameter space: bit-exact image and stats vs the reference, lossless
+    # round trip, and a randomly corrupted copy of each image failing with
+    # the reference's exact error (threads = 1 schedule)
+    rng = random.Random(2024)
+    kinds = ["quant", "runs", "alpha", "uniform", "periodic"]
+    for it in range(600):
+        S = rng.choice([1, 2, 4])
+        C = rng.choice([1024, 2048, 4096, 8192, 16384])
+        W = rng.choice([4, 5, 17, 32, 33, 64, 100, 128, 129, 200, 255])
+        W = min(W, C - 1)
+        I = rng.choice([1, 2, 4, 8, 16])
+        bb = C * S * rng.choice([1, 2, 3, 7, 64])
+        size = rng.choice([0, 1, S - 1, S, C * S - 1, C * S + 1, rng.randrange(1, 300000)])
+        size = max(0, size)
+        data = inputs.make(rng.choice(kinds), size, 1000 + it, S)
+        p = P(S, W, C, I, bb)
+        want, st = ref_compress(data, p)
+        stats = plz.PipelineStats()
+        got = plz.compress(data, p, stats=stats)
+        assert got == want, f"iteration {it}: S={S} W={W} C={C} I={I} bb={bb} n={size}"
+        assert (stats.pointer_tokens, stats.literal_tokens) == st[1:], f"iteration {it}"
+        assert plz.decompress_bytes(got) == data, f"iteration {it}"
+        if len(got) > 30:
+            bad = bytearray(got)
+            for _ in range(rng.choice([1, 2, 3])):
+                bad[rng.randrange(len(bad))] ^= rng.randrange(1, 256)
+            bad = bytes(bad)
+            assert _err(plz.decompress_bytes, bad) == _err(ref_decompress, bad), f"iteration {it}"
