@@ -88,34 +88,58 @@ constexpr int kTileX = 32, kTileY = 8;
 __global__ void __launch_bounds__(kTileX * kTileY) plz_lorenzo_tiled_kernel(
     const float* __restrict__ f, Dims g, float s, int32_t radius, uint16_t* __restrict__ codes,
     uint32_t* __restrict__ tile_count) {
+    constexpr int kHalo = (kTileY + 1) * (kTileX + 1);  // tile + row y0-1 + column x0-1
+    constexpr int kPlanes = 4;                           // planes loaded per round (in flight)
     __shared__ int32_t qs[kTileY + 1][kTileX + 1];
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t x = int64_t(blockIdx.x) * kTileX + tx, y = int64_t(blockIdx.y) * kTileY + ty;
     const bool in = x < int64_t(g.nx) && y < int64_t(g.ny);
+    // this thread's (at most two) halo slots: position in the tile, offset
+    // in a plane, and whether it lies in the field (q = 0 outside)
+    const int i0 = ty * kTileX + tx, i1 = i0 + kTileX * kTileY;
+    int hy[2], hx[2];
+    int64_t off[2];
+    bool val[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int i = k ? i1 : i0;
+        hy[k] = i / (kTileX + 1);
+        hx[k] = i % (kTileX + 1);
+        const int64_t gy = int64_t(blockIdx.y) * kTileY + hy[k] - 1;
+        const int64_t gx = int64_t(blockIdx.x) * kTileX + hx[k] - 1;
+        val[k] = i < kHalo && gy >= 0 && gx >= 0 && gy < int64_t(g.ny) && gx < int64_t(g.nx);
+        off[k] = val[k] ? gy * int64_t(g.nx) + gx : 0;
+    }
+    const bool has1 = i1 < kHalo;
+    const uint64_t plane_sz = g.ny * g.nx;
     int32_t prev = 0;  // the previous plane's 2-D term at (y, x)
-    for (uint64_t z = 0; z < g.nz; ++z) {
-        const float* plane = f + z * g.ny * g.nx;
-        // tile + halo (row y0-1, column x0-1), q = 0 outside the field
-        for (int i = ty * kTileX + tx; i < (kTileY + 1) * (kTileX + 1); i += kTileX * kTileY) {
-            const int hy = i / (kTileX + 1), hx = i % (kTileX + 1);
-            const int64_t gy = int64_t(blockIdx.y) * kTileY + hy - 1;
-            const int64_t gx = int64_t(blockIdx.x) * kTileX + hx - 1;
-            int32_t q = 0;
-            if (gy >= 0 && gx >= 0 && gy < int64_t(g.ny) && gx < int64_t(g.nx))
-                q = static_cast<int32_t>(rintf(__fmul_rn(__ldg(plane + gy * g.nx + gx), s)));
-            qs[hy][hx] = q;
+    for (uint64_t z0 = 0; z0 < g.nz; z0 += kPlanes) {
+        // kPlanes planes' loads issued together (memory-level parallelism),
+        // then each plane: tile into shared memory, 2-D term, z difference
+        float v[kPlanes][2];
+#pragma unroll
+        for (int d = 0; d < kPlanes; ++d)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+                v[d][k] = (val[k] && z0 + d < g.nz) ? __ldg(f + (z0 + d) * plane_sz + off[k]) : 0.f;
+#pragma unroll
+        for (int d = 0; d < kPlanes; ++d) {
+            const uint64_t z = z0 + d;
+            if (z >= g.nz) break;
+            qs[hy[0]][hx[0]] = val[0] ? static_cast<int32_t>(rintf(__fmul_rn(v[d][0], s))) : 0;
+            if (has1) qs[hy[1]][hx[1]] = val[1] ? static_cast<int32_t>(rintf(__fmul_rn(v[d][1], s))) : 0;
+            __syncthreads();
+            const int32_t cur = qs[ty + 1][tx + 1] - qs[ty + 1][tx] - qs[ty][tx + 1] + qs[ty][tx];
+            if (in) {
+                const int32_t dd = cur - prev;
+                const uint64_t i = (z * g.ny + uint64_t(y)) * g.nx + uint64_t(x);
+                const bool ok = dd > -radius && dd < radius;
+                codes[i] = ok ? uint16_t(dd + radius) : uint16_t(0);
+                if (!ok) atomicAdd(&tile_count[i / kQuantTile], 1u);
+            }
+            prev = cur;
+            __syncthreads();
         }
-        __syncthreads();
-        const int32_t cur = qs[ty + 1][tx + 1] - qs[ty + 1][tx] - qs[ty][tx + 1] + qs[ty][tx];
-        if (in) {
-            const int32_t d = cur - prev;
-            const uint64_t i = (z * g.ny + uint64_t(y)) * g.nx + uint64_t(x);
-            const bool ok = d > -radius && d < radius;
-            codes[i] = ok ? uint16_t(d + radius) : uint16_t(0);
-            if (!ok) atomicAdd(&tile_count[i / kQuantTile], 1u);
-        }
-        prev = cur;
-        __syncthreads();
     }
 }
 
@@ -187,9 +211,13 @@ __global__ void plz_scan_x_kernel(int32_t* __restrict__ d, uint64_t rows, uint64
          r += warps) {
         int32_t* row = d + r * nx;
         int32_t carry = 0;
+        // the next 32 elements are loaded before this step's store (the
+        // compiler cannot reorder the row's loads past its stores itself)
+        int32_t nxt = lane < nx ? row[lane] : 0;
         for (uint64_t x0 = 0; x0 < nx; x0 += 32) {
             const uint64_t x = x0 + lane;
-            int32_t v = x < nx ? row[x] : 0;
+            int32_t v = nxt;
+            nxt = x + 32 < nx ? row[x + 32] : 0;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
@@ -215,7 +243,21 @@ __global__ void plz_scan_strided_kernel(int32_t* __restrict__ d, uint64_t outer,
         const uint64_t o = c / stride, x = c % stride;
         const uint64_t b = o * outer_stride + x;
         int32_t run = 0;
-        for (uint64_t k = 0; k < len; ++k) {
+        // kBatch loads in flight per thread, then their running sums stored
+        constexpr int kBatch = 8;
+        uint64_t k = 0;
+        for (; k + kBatch <= len; k += kBatch) {
+            int32_t v[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) v[j] = d[b + (k + j) * stride];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                run += v[j];
+                if constexpr (kLast) f[b + (k + j) * stride] = __fmul_rn(float(run), two_eb);
+                else d[b + (k + j) * stride] = run;
+            }
+        }
+        for (; k < len; ++k) {
             run += d[b + k * stride];
             if constexpr (kLast) f[b + k * stride] = __fmul_rn(float(run), two_eb);
             else d[b + k * stride] = run;
