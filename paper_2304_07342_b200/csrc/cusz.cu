@@ -185,39 +185,40 @@ __global__ void __launch_bounds__(kQuantThreads) plz_outlier_write_kernel(
 }
 
 // ---- inverse
-// d = code - radius (0 for outliers), then the outlier residuals scattered
-__global__ void plz_codes_to_delta_kernel(const uint16_t* __restrict__ codes, uint64_t n,
-                                          int32_t radius, int32_t* __restrict__ d) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const int32_t c = codes[i];
-        d[i] = c ? c - radius : 0;
+// the residual of element i: code - radius, or (code 0) the outlier's value,
+// found by binary search in the index-ordered outlier list
+__device__ __forceinline__ int32_t residual(uint32_t code, uint64_t i, int32_t radius,
+                                            const uint64_t* __restrict__ idx,
+                                            const int32_t* __restrict__ val, uint64_t m) {
+    if (code) return int32_t(code) - radius;
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (idx[mid] < i) lo = mid + 1;
+        else hi = mid;
     }
+    return lo < m && idx[lo] == i ? val[lo] : 0;
 }
 
-__global__ void plz_outlier_scatter_kernel(const uint64_t* __restrict__ idx,
-                                           const int32_t* __restrict__ val, uint64_t m, uint64_t n,
-                                           int32_t* __restrict__ d) {
-    for (uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
-         j += uint64_t(gridDim.x) * blockDim.x)
-        if (idx[j] < n) d[idx[j]] = val[j];
-}
-
-// inclusive sums along x: one warp per row, 32 elements per step with a carry
-__global__ void plz_scan_x_kernel(int32_t* __restrict__ d, uint64_t rows, uint64_t nx) {
+// inclusive sums along x straight from the codes (residuals and outliers
+// resolved on the fly): one warp per row, 32 elements per step with a carry
+__global__ void plz_scan_x_codes_kernel(const uint16_t* __restrict__ codes, int32_t radius,
+                                        const uint64_t* __restrict__ idx,
+                                        const int32_t* __restrict__ val, uint64_t m,
+                                        int32_t* __restrict__ d, uint64_t rows, uint64_t nx) {
     const uint32_t lane = lane_id();
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t r = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows;
          r += warps) {
+        const uint16_t* crow = codes + r * nx;
         int32_t* row = d + r * nx;
         int32_t carry = 0;
-        // the next 32 elements are loaded before this step's store (the
-        // compiler cannot reorder the row's loads past its stores itself)
-        int32_t nxt = lane < nx ? row[lane] : 0;
+        uint32_t nxt = lane < nx ? crow[lane] : 1u;
         for (uint64_t x0 = 0; x0 < nx; x0 += 32) {
             const uint64_t x = x0 + lane;
-            int32_t v = nxt;
-            nxt = x + 32 < nx ? row[x + 32] : 0;
+            const uint32_t c = nxt;
+            nxt = x + 32 < nx ? crow[x + 32] : 1u;
+            int32_t v = x < nx ? residual(c, r * nx + x, radius, idx, val, m) : 0;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
@@ -308,9 +309,8 @@ void launch_lorenzo_reconstruct(const uint16_t* codes, const uint64_t* out_idx,
                                 int sms, cudaStream_t st) {
     const uint64_t n = nx * ny * nz;
     const unsigned grid = unsigned(sms) * 8;
-    plz_codes_to_delta_kernel<<<grid, 256, 0, st>>>(codes, n, radius, d);
-    if (n_out) plz_outlier_scatter_kernel<<<grid, 256, 0, st>>>(out_idx, out_val, n_out, n, d);
-    plz_scan_x_kernel<<<grid, 256, 0, st>>>(d, ny * nz, nx);
+    plz_scan_x_codes_kernel<<<grid, 256, 0, st>>>(codes, radius, out_idx, out_val, n_out, d,
+                                                  ny * nz, nx);
     // along y within each z-slab, then along z (which also dequantises)
     if (nz > 1) {
         if (ny > 1) plz_scan_strided_kernel<false><<<grid, 256, 0, st>>>(d, nz, ny, nx, nx * ny, two_eb, f);
@@ -323,15 +323,13 @@ void launch_lorenzo_reconstruct(const uint16_t* codes, const uint64_t* out_idx,
 }
 
 void preload_cusz_kernels() {
-    const void* fs[] = {reinterpret_cast<const void*>(plz_codes_to_delta_kernel),
-                          reinterpret_cast<const void*>(plz_dequant_kernel),
+    const void* fs[] = {reinterpret_cast<const void*>(plz_dequant_kernel),
                           reinterpret_cast<const void*>(plz_lorenzo_quant_kernel),
                           reinterpret_cast<const void*>(plz_lorenzo_tiled_kernel),
-                          reinterpret_cast<const void*>(plz_outlier_scatter_kernel),
                           reinterpret_cast<const void*>(plz_outlier_write_kernel),
                           reinterpret_cast<const void*>(plz_scan_strided_kernel<false>),
                           reinterpret_cast<const void*>(plz_scan_strided_kernel<true>),
-                          reinterpret_cast<const void*>(plz_scan_x_kernel)};
+                          reinterpret_cast<const void*>(plz_scan_x_codes_kernel)};
     for (const void* f : fs) preload_kernel(f);
 }
 
