@@ -16,4 +16,9 @@ for k in plz_scan plz_assemble plz_headers plz_parse plz_decode_kernel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/prof_${k}_$R python tools/probe.py c2 1 > /dev/null 2>&1
 done
+# the cuSZ use case: the quantizer's z-walk and the inverse's strided scan
+for k in plz_lorenzo_tiled plz_scan_strided; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+      -o gpurun_out/prof_${k}_$R python tools/cusz_pipeline.py --steps 1 > /dev/null 2>&1
+done
 ls -la gpurun_out
