@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kTileX * kTileY) plz_lorenzo_tiled_kernel(
     uint32_t* __restrict__ tile_count) {
     constexpr int kHalo = (kTileY + 1) * (kTileX + 1);  // tile + row y0-1 + column x0-1
     constexpr int kPlanes = 4;                           // planes loaded per round (in flight)
-    __shared__ int32_t qs[kTileY + 1][kTileX + 1];
+    __shared__ int32_t qs2[2][kTileY + 1][kTileX + 1];  // double-buffered: one barrier per plane
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t x = int64_t(blockIdx.x) * kTileX + tx, y = int64_t(blockIdx.y) * kTileY + ty;
     const bool in = x < int64_t(g.nx) && y < int64_t(g.ny);
@@ -126,6 +126,10 @@ __global__ void __launch_bounds__(kTileX * kTileY) plz_lorenzo_tiled_kernel(
         for (int d = 0; d < kPlanes; ++d) {
             const uint64_t z = z0 + d;
             if (z >= g.nz) break;
+            // plane z's tile goes to buffer z & 1: the barrier below also
+            // orders every read of plane z-1 (other buffer) before the
+            // writes of plane z+1 into it
+            int32_t (*qs)[kTileX + 1] = qs2[z & 1];
             qs[hy[0]][hx[0]] = val[0] ? static_cast<int32_t>(rintf(__fmul_rn(v[d][0], s))) : 0;
             if (has1) qs[hy[1]][hx[1]] = val[1] ? static_cast<int32_t>(rintf(__fmul_rn(v[d][1], s))) : 0;
             __syncthreads();
@@ -138,7 +142,6 @@ __global__ void __launch_bounds__(kTileX * kTileY) plz_lorenzo_tiled_kernel(
                 if (!ok) atomicAdd(&tile_count[i / kQuantTile], 1u);
             }
             prev = cur;
-            __syncthreads();
         }
     }
 }
