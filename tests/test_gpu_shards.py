@@ -104,3 +104,32 @@ def test_sharded_decompress_errors():
     with pytest.raises(plz.Error) as part:
         plz.decompress_range(th, 0, 1)
     assert type(part.value) is type(whole.value) and str(part.value) == str(whole.value)
+
+
+def test_decompress_range_with_host_buffers():
+    # the C-ABI range decode from a host image into a host buffer (staged
+    # through the context) equals the device-resident slices
+    import ctypes as C
+
+    p = plz.validate(plz.Params(2, 255, 2048, 2, 2048 * 2 * 4))
+    data = inputs.make("quant", 37 * 4096 + 5, 77, 2)
+    img = plz.compress(data, p)
+    ctx = plz.context()
+    src = C.create_string_buffer(img, len(img))
+    _, _, total = ctx.decompress_range(C.addressof(src), len(img), 0, 0, 0, 0)
+    at = 0
+    for b, e in dist.chunk_ranges(total, 3):
+        begin, ln, tot = ctx.decompress_range(C.addressof(src), len(img), b, e, 0, 0)
+        out = C.create_string_buffer(max(ln, 1))
+        begin2, ln2, _ = ctx.decompress_range(C.addressof(src), len(img), b, e, C.addressof(out),
+                                              ln)
+        assert (begin2, ln2, tot) == (begin, ln, total) and begin == at
+        assert out.raw[:ln] == data[begin:begin + ln]
+        at += ln
+    assert at == len(data)
+    # a buffer one byte short is the reference's capacity error
+    b, e = dist.chunk_ranges(total, 3)[1]
+    _, ln, _ = ctx.decompress_range(C.addressof(src), len(img), b, e, 0, 0)
+    small = C.create_string_buffer(ln)
+    with pytest.raises(plz.CapacityError):
+        ctx.decompress_range(C.addressof(src), len(img), b, e, C.addressof(small), ln - 1)
