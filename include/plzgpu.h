@@ -164,6 +164,17 @@ int plzgpu_decompress_range(plzgpu_ctx* ctx, const void* img, uint64_t len, uint
                             uint64_t* out_len, uint64_t* total_chunks, void* stream,
                             plzgpu_error* err);
 
+/* One stream compressed by several GPUs of this process (SURVEY.md §8b item
+ * 4: "a multi-GPU variant taking a device list"): chunk ranges encoded
+ * concurrently (one context and host thread per entry of `devices`; an entry
+ * may repeat a device), segments gathered into one image on devices[0] by
+ * peer copies, then copied to `out` (host or device).  The image equals
+ * plzgpu_compress's.  Replaces plz::compress (pipeline.hpp:28-30) for a
+ * device list; the one-process-per-GPU form is dist.compress_sharded. */
+int plzgpu_compress_multi(const int* devices, int n_devices, const plzgpu_params* params,
+                          const void* in, uint64_t n, void* out, uint64_t cap, uint64_t* out_len,
+                          plzgpu_stats* stats, plzgpu_error* err);
+
 /* Stream-ordered variant: device image and output; the decoded length lands
  * in *d_out_len.  Errors are reported by plzgpu_ctx_finish. */
 int plzgpu_decompress_async(plzgpu_ctx* ctx, const void* d_img, uint64_t len, void* d_out,

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <new>
 #include <string>
 #include <vector>
@@ -1954,6 +1955,175 @@ int plzgpu_pointer_histogram(plzgpu_ctx* c, const plzgpu_params* params, const v
     CK(cudaMemcpyAsync(hist, c->hist.p, 256 * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return PLZGPU_OK;
+}
+
+
+// One stream compressed by several GPUs of this process:
+// the shard protocol of dist.py with host threads for ranks — chunk ranges
+// encoded concurrently (one context and host thread per listed device), the
+// offset plan from the per-container totals, every rank's segments copied
+// into one image on the first device (peer copies), headers there, then the
+// image to `out`.  The image equals plzgpu_compress's byte for byte.
+int plzgpu_compress_multi(const int* devices, int n_devices, const plzgpu_params* params,
+                          const void* in, uint64_t n, void* out, uint64_t cap, uint64_t* out_len,
+                          plzgpu_stats* stats, plzgpu_error* err) {
+    clear_err(err);
+    *out_len = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    if (n_devices < 1 || !devices)
+        return set_err(err, PLZGPU_CONTRACT, 0, kNoIndex, kNoIndex, "empty device list");
+    if (n == 0) return PLZGPU_OK;
+    const plzgpu_params& p = *params;
+    const Geometry g = geometry(n, p);
+    const uint64_t S = uint64_t(p.symbol_width), C = uint64_t(p.chunk_size), N = uint64_t(n_devices);
+    const bool dev_in = is_device_ptr(in);
+    std::vector<plzgpu_ctx*> ctx(N, nullptr);
+    std::vector<void*> allocs;  // (device, pointer) pairs freed at the end
+    std::vector<int> alloc_dev;
+    auto cleanup = [&](int code) {
+        for (size_t i = 0; i < allocs.size(); ++i) {
+            cudaSetDevice(alloc_dev[i]);
+            cudaFree(allocs[i]);
+        }
+        for (plzgpu_ctx* c : ctx)
+            if (c) plzgpu_ctx_destroy(c);
+        return code;
+    };
+    auto dev_alloc = [&](int dev, uint64_t bytes, uint8_t** ptr) -> cudaError_t {
+        cudaError_t e = cudaSetDevice(dev);
+        if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(ptr), bytes);
+        if (e == cudaSuccess) {
+            allocs.push_back(*ptr);
+            alloc_dev.push_back(dev);
+        }
+        return e;
+    };
+    for (uint64_t r = 0; r < N; ++r) {
+        rc = plzgpu_ctx_create(devices[r], &ctx[r], err);
+        if (rc) return cleanup(rc);
+    }
+    // ---- ranks encode their chunk ranges concurrently
+    uint64_t max_touched = 1;
+    std::vector<uint64_t> rb(N), re(N);
+    for (uint64_t r = 0; r < N; ++r) {
+        rb[r] = g.n_chunks * r / N;
+        re[r] = g.n_chunks * (r + 1) / N;
+        max_touched = std::max(max_touched, (re[r] - rb[r] + g.cpb - 1) / g.cpb + 1);
+    }
+    std::vector<uint8_t*> slice(N, nullptr);
+    for (uint64_t r = 0; r < N; ++r) {  // a device input: each rank's slice onto its own GPU
+        const uint64_t lo = rb[r] * C * S, hi = re[r] == g.n_chunks ? n : re[r] * C * S;
+        if (!dev_in || hi <= lo) continue;
+        cudaError_t e = dev_alloc(devices[r], hi - lo, &slice[r]);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(slice[r], static_cast<const uint8_t*>(in) + lo, hi - lo, cudaMemcpyDefault);
+        if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi input"));
+    }
+    std::vector<std::vector<uint64_t>> tot(N);
+    std::vector<int> rcs(N, PLZGPU_OK);
+    std::vector<plzgpu_error> errs(N);
+    {
+        std::vector<std::thread> th;
+        for (uint64_t r = 0; r < N; ++r)
+            th.emplace_back([&, r] {
+                const void* src = slice[r] ? static_cast<const void*>(slice[r])
+                                           : static_cast<const uint8_t*>(in) + rb[r] * C * S;
+                tot[r].assign(3 * max_touched, 0);
+                uint64_t nt = 0;
+                rcs[r] = plzgpu_shard_encode(ctx[r], &p, src, n, rb[r], re[r], tot[r].data(),
+                                             max_touched, &nt, nullptr, &errs[r]);
+                tot[r].resize(3 * nt);
+            });
+        for (std::thread& t : th) t.join();
+    }
+    for (uint64_t r = 0; r < N; ++r)
+        if (rcs[r]) {
+            if (err) *err = errs[r];
+            return cleanup(rcs[r]);
+        }
+    // ---- the offset plan (dist.plan_offsets)
+    std::vector<uint64_t> ptot(g.n_blocks, 0), ftot(g.n_blocks, 0), img_off(g.n_blocks, 0);
+    std::vector<std::vector<uint64_t>> bases(N);
+    for (uint64_t r = 0; r < N; ++r)
+        for (size_t i = 0; 3 * i < tot[r].size(); ++i) {
+            const uint64_t j = tot[r][3 * i];
+            bases[r].insert(bases[r].end(), {ptot[j], ftot[j], 0, 0});
+            ptot[j] += tot[r][3 * i + 1];
+            ftot[j] += tot[r][3 * i + 2];
+        }
+    uint64_t image_len = 0;
+    for (uint64_t j = 0; j < g.n_blocks; ++j) {
+        const uint64_t nj = (j + 1 == g.n_blocks) ? g.n_chunks - j * g.cpb : g.cpb;
+        const uint64_t bytes = (j + 1 == g.n_blocks) ? n - j * p.block_bytes : p.block_bytes;
+        img_off[j] = image_len;
+        image_len += 26 + 8 * (nj + 1) + ptot[j] + ftot[j] + bytes % S;
+    }
+    for (uint64_t r = 0; r < N; ++r)
+        for (size_t i = 0; 3 * i < tot[r].size(); ++i) {
+            const uint64_t j = tot[r][3 * i];
+            bases[r][4 * i + 2] = img_off[j];
+            bases[r][4 * i + 3] = ftot[j];
+        }
+    if (image_len > cap)
+        return cleanup(set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                               "output buffer too small: need %llu bytes",
+                               (unsigned long long)image_len));
+    // ---- every rank's segments into one image on the first device
+    uint8_t* d_img = nullptr;
+    cudaError_t e = dev_alloc(devices[0], image_len + 16, &d_img);
+    if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi image"));
+    for (uint64_t r = 0; r < N; ++r) {
+        const uint64_t nt = tot[r].size() / 3;
+        if (nt == 0) continue;
+        uint64_t local = 8 * (re[r] - rb[r]) + 16;
+        for (uint64_t i = 0; i < nt; ++i) local += tot[r][3 * i + 1] + tot[r][3 * i + 2];
+        uint8_t* d_local = nullptr;
+        e = dev_alloc(devices[r], local, &d_local);
+        if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi segments"));
+        std::vector<uint64_t> segs(12 * nt);
+        uint64_t ns = 0, ln = 0;
+        rc = plzgpu_shard_assemble(ctx[r], bases[r].data(), d_local, local, segs.data(), 4 * nt,
+                                   &ns, &ln, nullptr, err);
+        if (rc) return cleanup(rc);
+        for (uint64_t k = 0; k < ns; ++k)
+            if (segs[3 * k + 2]) {
+                e = cudaMemcpy(d_img + segs[3 * k], d_local + segs[3 * k + 1], segs[3 * k + 2],
+                               cudaMemcpyDefault);
+                if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi gather"));
+            }
+    }
+    // ---- headers, final table entries and the tail on the root, then out
+    std::vector<uint64_t> totals(2 * g.n_blocks);
+    for (uint64_t j = 0; j < g.n_blocks; ++j) {
+        totals[2 * j] = ptot[j];
+        totals[2 * j + 1] = ftot[j];
+    }
+    uint8_t tail[4] = {0, 0, 0, 0};
+    const uint64_t tl = n % S;
+    if (tl) {
+        e = cudaMemcpy(tail, static_cast<const uint8_t*>(in) + (n - tl), tl, cudaMemcpyDefault);
+        if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi tail"));
+    }
+    uint64_t img_len = 0;
+    rc = plzgpu_shard_headers(ctx[0], &p, n, totals.data(), tail, d_img, image_len + 16, &img_len,
+                              nullptr, err);
+    if (rc) return cleanup(rc);
+    e = cudaMemcpy(out, d_img, img_len, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_compress_multi output"));
+    if (stats) {
+        for (uint64_t r = 0; r < N; ++r) {
+            unsigned long long st2[2] = {0, 0};
+            cudaSetDevice(devices[r]);
+            if (cudaMemcpy(st2, dmeta(ctx[r])->stats, sizeof st2, cudaMemcpyDeviceToHost) == cudaSuccess) {
+                stats->pointer_tokens += st2[0];
+                stats->literal_tokens += st2[1];
+            }
+        }
+    }
+    *out_len = img_len;
+    return cleanup(PLZGPU_OK);
 }
 
 }  // extern "C"

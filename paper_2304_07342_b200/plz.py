@@ -16,7 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import threading
 from dataclasses import dataclass
-from typing import List, Optional, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 from . import _lib as L
 
@@ -378,6 +378,39 @@ def decompress_bytes(img, threads: int = 0):
     out = C.create_string_buffer(max(cap, 1))
     ln = ctx.decompress_ptr(ptr, n, C.addressof(out), cap)
     return out.raw[:ln]
+
+
+def compress_multi(data, params: Params, devices: Sequence[int],
+                   stats: Optional[PipelineStats] = None):
+    """plz::compress of one stream on several GPUs of this process
+    (plzgpu_compress_multi): chunk-range shards, one per entry of `devices`;
+    the image equals compress(data, params).  Host input -> bytes, CUDA
+    tensor -> CUDA uint8 tensor on devices[0]."""
+    devs = (C.c_int * len(devices))(*devices)
+    e, st, ln = L.Error(), L.Stats(), C.c_uint64()
+    if _is_torch(data) and data.is_cuda:
+        import torch
+
+        t = data.contiguous().view(torch.uint8).reshape(-1)
+        cap = compress_bound(t.numel(), params)
+        out = torch.empty(max(cap, 16), dtype=torch.uint8, device=torch.device("cuda", devices[0]))
+        _check(L.lib().plzgpu_compress_multi(devs, len(devices), C.byref(params.to_c()),
+                                             C.c_void_p(t.data_ptr()), t.numel(),
+                                             C.c_void_p(out.data_ptr()), out.numel(), C.byref(ln),
+                                             C.byref(st), C.byref(e)), e)
+        res = out[:ln.value]
+    else:
+        ptr, n, keep = _as_host(data)
+        cap = compress_bound(n, params)
+        out = C.create_string_buffer(max(cap, 1))
+        _check(L.lib().plzgpu_compress_multi(devs, len(devices), C.byref(params.to_c()),
+                                             C.c_void_p(ptr), n, C.addressof(out), cap, C.byref(ln),
+                                             C.byref(st), C.byref(e)), e)
+        res = out.raw[:ln.value]
+    if stats is not None:
+        stats.pointer_tokens += st.pointer_tokens
+        stats.literal_tokens += st.literal_tokens
+    return res
 
 
 def decompress_range(img, chunk_begin: int, chunk_end: int):

@@ -133,3 +133,25 @@ def test_decompress_range_with_host_buffers():
     small = C.create_string_buffer(ln)
     with pytest.raises(plz.CapacityError):
         ctx.decompress_range(C.addressof(src), len(img), b, e, C.addressof(small), ln - 1)
+
+
+# ------------------------------------------- one process, a device list
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0, 0]])
+@pytest.mark.parametrize("S,W,C,I,bb", [(2, 255, 2048, 2, 2048 * 2 * 5), (1, 128, 4096, 1, 4096 * 3),
+                                        (4, 64, 1024, 4, 256 << 20)])
+def test_compress_multi_equals_single_call(devices, S, W, C, I, bb):
+    # plzgpu_compress_multi (device list; a repeated device = another context
+    # and host thread on it): host and device inputs, tails, ranges cutting
+    # containers; the image and stats equal the single call's
+    import torch
+
+    p = plz.validate(plz.Params(S, W, C, I, bb))
+    data = inputs.make("quant", 23 * C * S + 3 * S + (S - 1), 300 + len(devices), S)
+    st1, st2 = plz.PipelineStats(), plz.PipelineStats()
+    want = plz.compress(data, p, stats=st1)
+    got = plz.compress_multi(data, p, devices, stats=st2)
+    assert got == want
+    assert (st2.pointer_tokens, st2.literal_tokens) == (st1.pointer_tokens, st1.literal_tokens)
+    d = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    got_d = plz.compress_multi(d, p, devices)
+    assert got_d.is_cuda and bytes(got_d.cpu().numpy().tobytes()) == want
