@@ -175,6 +175,13 @@ int plzgpu_compress_multi(const int* devices, int n_devices, const plzgpu_params
                           const void* in, uint64_t n, void* out, uint64_t cap, uint64_t* out_len,
                           plzgpu_stats* stats, plzgpu_error* err);
 
+/* One image decompressed by several GPUs of this process: rank r decodes the
+ * global chunk range r (plzgpu_decompress_range) on devices[r] and its slice
+ * lands at its offset in `out` (host or device).  Output and errors equal
+ * plzgpu_decompress's. */
+int plzgpu_decompress_multi(const int* devices, int n_devices, const void* img, uint64_t len,
+                            void* out, uint64_t cap, uint64_t* out_len, plzgpu_error* err);
+
 /* Stream-ordered variant: device image and output; the decoded length lands
  * in *d_out_len.  Errors are reported by plzgpu_ctx_finish. */
 int plzgpu_decompress_async(plzgpu_ctx* ctx, const void* d_img, uint64_t len, void* d_out,

@@ -73,6 +73,8 @@ SIGNATURES = [  # every entry point of include/plzgpu.h
     ("plzgpu_decompress_async", C.c_int, [_VP, _VP, _U64, _VP, _U64, _VP, _VP, _E]),
     ("plzgpu_compress_multi", C.c_int, [C.POINTER(C.c_int), C.c_int, _P, _VP, _U64, _VP, _U64,
                                         C.POINTER(_U64), C.POINTER(Stats), _E]),
+    ("plzgpu_decompress_multi", C.c_int, [C.POINTER(C.c_int), C.c_int, _VP, _U64, _VP, _U64,
+                                          C.POINTER(_U64), _E]),
     ("plzgpu_decompress_range", C.c_int, [_VP, _VP, _U64, _U64, _U64, _VP, _U64, C.POINTER(_U64),
                                           C.POINTER(_U64), C.POINTER(_U64), _VP, _E]),
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),

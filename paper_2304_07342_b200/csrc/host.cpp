@@ -2126,4 +2126,116 @@ int plzgpu_compress_multi(const int* devices, int n_devices, const plzgpu_params
     return cleanup(PLZGPU_OK);
 }
 
+
+// One image decompressed by several GPUs of this process: rank r decodes the
+// global chunk range r (plzgpu_decompress_range) on its own device, from a
+// copy of the image there when the image is another device's memory, and
+// its slice is copied to its offset in `out`.  The first failing rank's
+// error is the single call's (ranks are in chunk order; header errors are
+// every rank's).
+int plzgpu_decompress_multi(const int* devices, int n_devices, const void* img, uint64_t len,
+                            void* out, uint64_t cap, uint64_t* out_len, plzgpu_error* err) {
+    clear_err(err);
+    *out_len = 0;
+    if (n_devices < 1 || !devices)
+        return set_err(err, PLZGPU_CONTRACT, 0, kNoIndex, kNoIndex, "empty device list");
+    if (len == 0) return PLZGPU_OK;
+    const uint64_t N = uint64_t(n_devices);
+    int img_dev = -1;
+    {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, img) == cudaSuccess && at.type == cudaMemoryTypeDevice)
+            img_dev = at.device;
+        else
+            cudaGetLastError();
+    }
+    std::vector<plzgpu_ctx*> ctx(N, nullptr);
+    std::vector<void*> allocs;
+    std::vector<int> alloc_dev;
+    auto cleanup = [&](int code) {
+        for (size_t i = 0; i < allocs.size(); ++i) {
+            cudaSetDevice(alloc_dev[i]);
+            cudaFree(allocs[i]);
+        }
+        for (plzgpu_ctx* c : ctx)
+            if (c) plzgpu_ctx_destroy(c);
+        return code;
+    };
+    for (uint64_t r = 0; r < N; ++r) {
+        const int rc = plzgpu_ctx_create(devices[r], &ctx[r], err);
+        if (rc) return cleanup(rc);
+    }
+    // the image each rank reads: the caller's (host, or on the rank's device)
+    // or a copy on the rank's device
+    std::vector<const void*> src(N, img);
+    for (uint64_t r = 0; r < N; ++r) {
+        if (img_dev < 0 || img_dev == devices[r]) continue;
+        void* p = nullptr;
+        cudaError_t e = cudaSetDevice(devices[r]);
+        if (e == cudaSuccess) e = cudaMalloc(&p, len);
+        if (e == cudaSuccess) {
+            allocs.push_back(p);
+            alloc_dev.push_back(devices[r]);
+            e = cudaMemcpy(p, img, len, cudaMemcpyDefault);
+        }
+        if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_decompress_multi image"));
+        src[r] = p;
+    }
+    uint64_t b0 = 0, l0 = 0, total = 0;
+    int rc = plzgpu_decompress_range(ctx[0], src[0], len, 0, 0, nullptr, 0, &b0, &l0, &total,
+                                     nullptr, err);
+    if (rc) return cleanup(rc);
+    std::vector<int> rcs(N, PLZGPU_OK);
+    std::vector<plzgpu_error> errs(N);
+    std::vector<uint64_t> begin(N, 0), size(N, 0);
+    std::vector<uint8_t*> slice(N, nullptr);
+    std::mutex mu;  // allocation bookkeeping
+    {
+        std::vector<std::thread> th;
+        for (uint64_t r = 0; r < N; ++r)
+            th.emplace_back([&, r] {
+                const uint64_t cb = total * r / N, ce = total * (r + 1) / N;
+                uint64_t tc = 0;
+                rcs[r] = plzgpu_decompress_range(ctx[r], src[r], len, cb, ce, nullptr, 0, &begin[r],
+                                                 &size[r], &tc, nullptr, &errs[r]);
+                if (rcs[r] || size[r] == 0) return;
+                void* p = nullptr;
+                cudaError_t e = cudaSetDevice(devices[r]);
+                if (e == cudaSuccess) e = cudaMalloc(&p, size[r] + 16);
+                if (e != cudaSuccess) {
+                    rcs[r] = cuda_fail(&errs[r], e, "plzgpu_decompress_multi slice");
+                    return;
+                }
+                {
+                    std::lock_guard<std::mutex> lock(mu);
+                    allocs.push_back(p);
+                    alloc_dev.push_back(devices[r]);
+                }
+                slice[r] = static_cast<uint8_t*>(p);
+                uint64_t b2 = 0, l2 = 0;
+                rcs[r] = plzgpu_decompress_range(ctx[r], src[r], len, cb, ce, p, size[r] + 16, &b2,
+                                                 &l2, &tc, nullptr, &errs[r]);
+            });
+        for (std::thread& t : th) t.join();
+    }
+    for (uint64_t r = 0; r < N; ++r)
+        if (rcs[r]) {
+            if (err) *err = errs[r];
+            return cleanup(rcs[r]);
+        }
+    const uint64_t total_out = begin[N - 1] + size[N - 1];
+    if (total_out > cap)
+        return cleanup(set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
+                               "output buffer too small: need %llu bytes",
+                               (unsigned long long)total_out));
+    for (uint64_t r = 0; r < N; ++r)
+        if (size[r]) {
+            const cudaError_t e = cudaMemcpy(static_cast<uint8_t*>(out) + begin[r], slice[r], size[r],
+                                             cudaMemcpyDefault);
+            if (e != cudaSuccess) return cleanup(cuda_fail(err, e, "plzgpu_decompress_multi output"));
+        }
+    *out_len = total_out;
+    return cleanup(PLZGPU_OK);
+}
+
 }  // extern "C"

@@ -413,6 +413,31 @@ def compress_multi(data, params: Params, devices: Sequence[int],
     return res
 
 
+def decompress_multi(img, devices: Sequence[int]):
+    """plz::decompress_bytes on several GPUs of this process
+    (plzgpu_decompress_multi): bytes in -> bytes out, CUDA tensor in -> CUDA
+    uint8 tensor on devices[0]."""
+    devs = (C.c_int * len(devices))(*devices)
+    e, ln = L.Error(), C.c_uint64()
+    if _is_torch(img) and img.is_cuda:
+        import torch
+
+        t = img.contiguous().view(torch.uint8).reshape(-1)
+        cap = context().decompressed_size(t.data_ptr(), t.numel(),
+                                          torch.cuda.current_stream(t.device).cuda_stream)
+        out = torch.empty(max(cap, 16), dtype=torch.uint8, device=torch.device("cuda", devices[0]))
+        _check(L.lib().plzgpu_decompress_multi(devs, len(devices), C.c_void_p(t.data_ptr()),
+                                               t.numel(), C.c_void_p(out.data_ptr()), out.numel(),
+                                               C.byref(ln), C.byref(e)), e)
+        return out[:ln.value]
+    ptr, n, keep = _as_host(img)
+    cap = int(L.lib().plzgpu_decompressed_bound(C.c_void_p(ptr), n))
+    out = C.create_string_buffer(max(cap, 1))
+    _check(L.lib().plzgpu_decompress_multi(devs, len(devices), C.c_void_p(ptr), n,
+                                           C.addressof(out), cap, C.byref(ln), C.byref(e)), e)
+    return out.raw[:ln.value]
+
+
 def decompress_range(img, chunk_begin: int, chunk_end: int):
     """Decodes the global chunks [chunk_begin, chunk_end) of a CUDA image
     tensor: returns (output slice tensor, its offset in the decompressed

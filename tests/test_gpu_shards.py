@@ -155,3 +155,32 @@ def test_compress_multi_equals_single_call(devices, S, W, C, I, bb):
     d = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
     got_d = plz.compress_multi(d, p, devices)
     assert got_d.is_cuda and bytes(got_d.cpu().numpy().tobytes()) == want
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0, 0, 0]])
+def test_decompress_multi_equals_single_call(devices):
+    import torch
+
+    parts = [inputs.make("alpha", k, k, 4) for k in (4099, 3, 12345, 70001)]
+    p = plz.validate(plz.Params(4, 255, 1024, 2, 1024 * 4 * 3))
+    img = b"".join(plz.compress(d, p) for d in parts)
+    want = b"".join(parts)
+    assert plz.decompress_multi(img, devices) == want
+    t = torch.frombuffer(bytearray(img), dtype=torch.uint8).cuda()
+    got = plz.decompress_multi(t, devices)
+    assert got.is_cuda and bytes(got.cpu().numpy().tobytes()) == want
+    # a corrupt chunk: the single call's error, whichever rank holds it
+    bad = bytearray(img)
+    bad[len(bad) // 2] ^= 0xFF
+    bad[len(bad) // 2 + 7] ^= 0x3C
+    try:
+        plz.decompress_bytes(bytes(bad))
+        w = None
+    except plz.Error as e:
+        w = (type(e), str(e))
+    try:
+        plz.decompress_multi(bytes(bad), devices)
+        g = None
+    except plz.Error as e:
+        g = (type(e), str(e))
+    assert g == w
