@@ -18,6 +18,7 @@
 #include "plz/params.hpp"
 #include "plz/pipeline.hpp"
 #include "plz/tuner.hpp"
+#include "plzgpu.h"
 
 namespace {
 
@@ -147,12 +148,53 @@ void append_csv(const std::string& path, const std::string& rows) {
     out << rows;
 }
 
+// --gpus 0,1,...: one stream over a device list (plzgpu_compress_multi /
+// plzgpu_decompress_multi); errors mapped like the C++ API's
+void throw_gpu_error(int rc, const plzgpu_error& e) {
+    const std::string msg = e.message;
+    switch (rc) {
+        case PLZGPU_VALIDATION: throw plz::validation_error(msg);
+        case PLZGPU_UNSUPPORTED_FORMAT: throw plz::unsupported_format_error(msg);
+        case PLZGPU_CORRUPTION: throw plz::corruption_error(msg, e.byte_offset);
+        default: throw plz::error(msg);
+    }
+}
+
+std::vector<int> g_devices;  // set by --gpus
+
+std::vector<std::uint8_t> compress_on(const std::vector<std::uint8_t>& data, const plz::Params& p,
+                                      int threads) {
+    if (g_devices.empty()) return plz::compress(data, p, threads);
+    plzgpu_params cp{p.symbol_width, p.window, p.chunk_size, p.interval,
+                     uint64_t(p.block_bytes), p.min_match, 0};
+    std::vector<std::uint8_t> out(plzgpu_compress_bound(data.size(), &cp) + 16);
+    uint64_t n = 0;
+    plzgpu_error e{};
+    const int rc = plzgpu_compress_multi(g_devices.data(), int(g_devices.size()), &cp, data.data(),
+                                         data.size(), out.data(), out.size(), &n, nullptr, &e);
+    if (rc) throw_gpu_error(rc, e);
+    out.resize(n);
+    return out;
+}
+
+std::vector<std::uint8_t> decompress_on(const std::vector<std::uint8_t>& img) {
+    if (g_devices.empty()) return plz::decompress_bytes(img);
+    std::vector<std::uint8_t> out(plzgpu_decompressed_bound(img.data(), img.size()) + 16);
+    uint64_t n = 0;
+    plzgpu_error e{};
+    const int rc = plzgpu_decompress_multi(g_devices.data(), int(g_devices.size()), img.data(),
+                                           img.size(), out.data(), out.size(), &n, &e);
+    if (rc) throw_gpu_error(rc, e);
+    out.resize(n);
+    return out;
+}
+
 // wall time around plz::compress only (tools/plz.cpp:115-131)
 RunReport timed_compress(const std::string& name, const std::vector<std::uint8_t>& data,
                          const plz::Params& p, int threads, std::vector<std::uint8_t>* out) {
     RunReport r{name, p, threads, data.size(), 0, 0};
     const auto t0 = std::chrono::steady_clock::now();
-    std::vector<std::uint8_t> img = plz::compress(data, p, threads);
+    std::vector<std::uint8_t> img = compress_on(data, p, threads);
     r.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     r.out_bytes = img.size();
     if (out) *out = std::move(img);
@@ -184,9 +226,10 @@ int run(int argc, char** argv) {
     const std::string cmd = argv[1];
     if (cmd == "compress") {
         std::vector<std::string> opts = kParamOpts;
-        opts.insert(opts.end(), {"--threads", "--csv"});
+        opts.insert(opts.end(), {"--threads", "--csv", "--gpus"});
         const Args a(argc, argv, 2, opts, {});
         if (a.pos.size() != 2) throw UsageError("compress needs input and output paths");
+        if (a.has("--gpus")) g_devices = parse_list<int>(a.opt.at("--gpus"), "--gpus");
         const plz::Params p = params_from(a);
         const int threads = int(to_int(a.get("--threads", "--threads", "0"), "--threads"));
         const std::vector<std::uint8_t> data = read_file(a.pos[0]);
@@ -198,11 +241,12 @@ int run(int argc, char** argv) {
         return 0;
     }
     if (cmd == "decompress") {
-        const Args a(argc, argv, 2, {"--threads"}, {});
+        const Args a(argc, argv, 2, {"--threads", "--gpus"}, {});
         if (a.pos.size() != 2) throw UsageError("decompress needs input and output paths");
+        if (a.has("--gpus")) g_devices = parse_list<int>(a.opt.at("--gpus"), "--gpus");
         const std::vector<std::uint8_t> data = read_file(a.pos[0]);
         try {
-            write_file(a.pos[1], plz::decompress_bytes(data));
+            write_file(a.pos[1], decompress_on(data));
         } catch (const plz::corruption_error& e) {
             std::cerr << "error: " << e.what() << '\n';
             return 3;

@@ -116,6 +116,17 @@ def test_cli_mirrors_reference_cli(tmp_path):
     assert _cli("compress", "-W", 0, src, tmp_path / "x.plz").returncode == 2
     (tmp_path / "garbage.plz").write_bytes(b"XXXXnot a container at all")
     assert _cli("decompress", tmp_path / "garbage.plz", tmp_path / "y.bin").returncode == 3
+    # --gpus: the same file from a device list (here the one GPU, three ranks)
+    assert _cli("compress", "-S", 2, "-W", 128, "-C", 2048, "--block-bytes", 16384, "--gpus",
+                "0,0,0", src, tmp_path / "multi.plz").returncode == 0
+    assert _cli("compress", "-S", 2, "-W", 128, "-C", 2048, "--block-bytes", 16384, src,
+                tmp_path / "single.plz").returncode == 0
+    assert (tmp_path / "multi.plz").read_bytes() == (tmp_path / "single.plz").read_bytes()
+    assert _cli("decompress", "--gpus", "0,0", tmp_path / "multi.plz",
+                tmp_path / "mback.bin").returncode == 0
+    assert (tmp_path / "mback.bin").read_bytes() == src.read_bytes()
+    assert _cli("decompress", "--gpus", "0,0", tmp_path / "garbage.plz",
+                tmp_path / "y.bin").returncode == 3
     r = _cli("stats", "-S", 1, src)
     assert r.returncode == 0 and "length,count,byte_length,fraction_gt_128,fraction_gt_256" in r.stdout
     r = _cli("tune", "--declared-width", 2, src)
