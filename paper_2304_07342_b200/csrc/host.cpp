@@ -762,6 +762,7 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     const uint64_t seg_out = uint64_t(env_int("PLZGPU_DSEG_OUT_MB", 32)) << 20;
     const uint64_t kLead = uint64_t(env_int("PLZGPU_DSEG_LEAD", 1));
     const uint64_t kGroup = uint64_t(env_int("PLZGPU_DSEG_GROUP", 1));
+    const uint64_t kGroupOut = uint64_t(env_int("PLZGPU_DSEG_GROUP_OUT", int(kGroup)));
     StreamWriteValue32Fn write_value = stream_write_value32();
     StreamWaitValue32Fn wait_value = stream_wait_value32();
     if (!write_value || !wait_value || getenv_flag("PLZGPU_NO_PIPE_DEC") || getenv_flag("PLZGPU_NO_PIPE"))
@@ -887,7 +888,7 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
     for (uint64_t sg = 0; sg < nseg_out;) {
-        const uint64_t s_end = std::min(nseg_out, sg + (sg < kLead ? 1 : kGroup));
+        const uint64_t s_end = std::min(nseg_out, sg + (sg < kLead ? 1 : kGroupOut));
         const uint64_t lo = sg * seg_out, hi = std::min(total_out, s_end * seg_out);
         for (; sg < s_end; ++sg)
             if (wait_value(c->asm_stream, reinterpret_cast<unsigned long long>(pp.out_done + sg),
