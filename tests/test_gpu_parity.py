@@ -164,15 +164,16 @@ def test_bitmap_passes_in_sequence_on_a_large_input():
     # Inputs with many chunks per resident warp run the 16/32/64-row bitmap
     # passes one after the other (each takes the previous one's overflow);
     # small inputs sort the overflow first and run the 32/64-row passes side
-    # by side.  A large input mixing alphabets of 7, 20, 40 and 100 symbols
-    # per chunk exercises the sequential order; reference image required.
+    # by side.  A large input mixing alphabets of 7 .. 100 symbols per chunk
+    # (on both sides of the 16 / 32 / 64-row boundaries) exercises the
+    # sequential order; reference image required.
     import numpy as np
 
     rng = np.random.default_rng(77)
     S, C = 2, 2048
     chunks = []
     for k in range(20480):
-        d = (7, 20, 40, 100)[k % 4]
+        d = (7, 16, 17, 20, 24, 25, 32, 33, 40, 64, 65, 100)[k % 12]
         alphabet = rng.permutation(1024)[:d].astype("<u2") + 32000
         idx = np.repeat(rng.integers(0, d, C), rng.integers(1, 4, C))[:C]
         idx[:d] = np.arange(d)
