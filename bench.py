@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-mib", type=int, default=64)
+    ap.add_argument("--interval", type=int, default=0,
+                    help="reference arm only: override the workload's interval I")
     return ap.parse_args()
 
 
@@ -154,7 +156,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- reference arm
-def cpu_reference(workload, steps, warmup, sample_mib, quiet=False):
+def cpu_reference(workload, steps, warmup, sample_mib, quiet=False, interval=None):
     """The reference library (oracle/_ref, compiled from its own sources) on all
     host cores over a bounded prefix of the workload; returns GB/s figures."""
     import numpy as np
@@ -169,7 +171,7 @@ def cpu_reference(workload, steps, warmup, sample_mib, quiet=False):
     host = np.ascontiguousarray(data[:n].cpu().numpy())
     del data
     cores = os.cpu_count() or 1
-    p = O.make_params(w.S, w.W, w.C, w.I)
+    p = O.make_params(w.S, w.W, w.C, interval or w.I)
     kind = "reference" if O.ref_available() else "port"
     ptr = host.ctypes.data
     if kind == "reference":
@@ -209,7 +211,7 @@ def run_reference_arm(args):
     w = datagen.WORKLOADS[args.workload]
     try:
         r = cpu_reference(args.workload, max(1, args.steps), max(0, min(args.warmup, 1)),
-                          args.cpu_sample_mib)
+                          args.cpu_sample_mib, interval=args.interval or None)
     except FileNotFoundError as e:
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return 0
@@ -218,7 +220,7 @@ def run_reference_arm(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["sample_bytes"] / r["compress_gbs"] / 1e6,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"u{8 * w.S}",
         "data": "synthetic cuSZ-style quant codes (seed 42)", "impl": "reference",
-        "config": {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": w.I,
+        "config": {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": args.interval or w.I,
                    "bytes_per_step": r["sample_bytes"], "parallelism": "host threads"},
         "ratio": r["ratio"],
         "decompress": {"value": r["decompress_gbs"], "unit": "GB/s"},

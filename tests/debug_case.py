@@ -1,4 +1,4 @@
-"""Debug aid: compress one golden case on the GPU and report the first token
+"""Debug aid (test infrastructure, not collected): compress one golden case on the GPU and report the first token
 that differs from the C oracle (position, oracle match, GPU token)."""
 import json
 import sys

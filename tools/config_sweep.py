@@ -10,21 +10,20 @@ c5  u16 8 GiB (32 NYX-like fields), W=255, I=2, one GPU
 
 One JSON line per (config, I): compress / decompress GB/s of input bytes
 (device-resident, CUDA events, warm-up first, inputs > L2 except c1), ratio,
-round-trip check.  --cpu adds the reference library (oracle/_ref, all host
-threads) on the first 16 MiB of each config for the ratio/throughput beside
-it (test infrastructure: the CPU checker, not the measured path).
+round-trip check.  --cpu adds the reference library on all host threads over
+the first 16 MiB of each config (bench.py --impl reference), for the ratio /
+throughput beside it.
 """
 import argparse
 import json
 import os
+import subprocess
 import sys
-import time
 
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "oracle"))
 from paper_2304_07342_b200 import datagen, plz  # noqa: E402
 
 
@@ -78,22 +77,19 @@ def run(ctx, d_in, params, steps):
             "pointer_tokens": ptr, "literal_tokens": lit, "roundtrip_ok": ok}
 
 
-def cpu_ref(d_in, params):
-    import numpy as np
-
-    import oracle as O
-
-    if not O.ref_available():
+def cpu_ref(name, I):
+    """The reference library on all host cores over the first 16 MiB, through
+    bench.py's reference arm (the one place outside tests/ that runs oracle/)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", name, "--interval", str(I), "--steps", "2", "--warmup", "0",
+                        "--cpu-sample-mib", "16"], capture_output=True, text=True)
+    try:
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"cpu_compress_gbs": d["value"], "cpu_ratio": d["ratio"],
+                "cpu_cores": d["cpu_baseline"]["cores"],
+                "cpu_sample_bytes": d["config"]["bytes_per_step"]}
+    except (IndexError, KeyError, ValueError):
         return None
-    n = min(d_in.numel(), 16 << 20)
-    host = np.ascontiguousarray(d_in[:n].cpu().numpy())
-    p = O.make_params(params.symbol_width, params.window, params.chunk_size, params.interval)
-    cores = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    ln = O.ref_compress_into(host.ctypes.data, n, p, cores)
-    t = time.perf_counter() - t0
-    return {"cpu_compress_gbs": n / t / 1e9, "cpu_ratio": n / ln, "cpu_cores": cores,
-            "cpu_sample_bytes": n}
 
 
 def main():
@@ -112,7 +108,7 @@ def main():
             line = {"config": name, "workload": w.name, "bytes": d_in.numel(), "S": w.S,
                     "W": w.W, "C": w.C, "I": I, **r}
             if args.cpu:
-                line.update(cpu_ref(d_in, params) or {})
+                line.update(cpu_ref(name, I) or {})
             print(json.dumps(line), flush=True)
         del d_in
         torch.cuda.empty_cache()
