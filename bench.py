@@ -1,35 +1,42 @@
 """bench.py — GPULZ compress/decompress throughput on B200 (the driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload c2] [--no-cpu-baseline]
+                    [--workload c5] [--no-cpu-baseline]
 
-Workload: BASELINE.json configs[1] (c2): synthetic cuSZ-style uint16 quant
-codes, CESM-ATM-like 26x1800x3600 (336,960,000 B), radius 512, S=2, W=255
-("window 256" is capped at 255 by params.cpp:22-23), C=2048 symbols (4096-B
-chunks), I=2.  One step = one compress of the rank's whole input with the
-input already in HBM; decompress of the produced image is timed the same way
-and reported beside it.  Inputs (337 MB) exceed the 126 MB L2, so no flush is
-needed between steps.
+Workload (BASELINE.json's metric "... at 1/2/4/8 B200"): config c5, the 8 GiB
+synthetic cuSZ-style u16 quant-code stream — 32 NYX-like 512^3 fields, seeds
+42+k, one 256 MiB container each — S=2, W=255 ("window 256"
+is capped at 255 by params.cpp:22-23), C=2048 symbols (4096-B chunks), I=2.
+One step = one compress of the WHOLE 8 GiB stream with the input already in
+HBM; the decompress of the produced image is timed the same way and
+reported beside it.  Inputs (8 GiB) exceed the 126 MB L2: no flush needed.
 
-value      = compress GB/s of input bytes, whole job (sum over ranks / max time)
-e2e        = the same through the public C-ABI call with HOST buffers (pinned
-             input H2D + image D2H inside the timed region)
-roofline   = Kernel I (plz_bitmatch_kernel, the dominant kernel): algorithmic
-             bytes (input read + staged tokens written) / its CUDA-event time
-cpu_baseline = oracle/_ref (the reference library) on this host's cores
+N>1 (torchrun, NCCL): STRONG scaling — the same 8 GiB stream is split into
+contiguous chunk ranges (dist.chunk_ranges), rank r holding only its range;
+the timed step is the sharded compress of SURVEY.md §8e (dist.py): Kernels
+I+II per rank, one NCCL all-gather of per-container sizes, rebased
+table/stream segments per rank, P2P gather into ONE image on rank 0 that is
+byte-identical to the single-GPU image.  value = 8 GiB / max-over-ranks time.
 
-N>1 (torchrun, NCCL): weak scaling — the global input is the union of the
-ranks' c2-sized fields (seed 42+r); rank r holds chunk range r of its
-partition and the timed step is the sharded compress of SURVEY.md §8e
-(paper_2304_07342_b200/dist.py): Kernels I+II per rank, one NCCL all-gather of
-per-container sizes, per-rank rebased table/stream segments, P2P gather into
-one image on rank 0 that is byte-identical to a single-GPU compress.
-BENCH_DIST_BACKEND=gloo runs the same path with several ranks on one GPU
-(host-staged exchanges) to exercise it without a multi-GPU box.
+value        = compress GB/s of input bytes, whole job
+e2e          = the same through the public C-ABI call (plzgpu_compress /
+               plzgpu_decompress) with pinned HOST buffers, H2D + D2H inside
+               the timed region; e2e.pageable = the same with pageable
+               (malloc'd) buffers, the path a std::vector caller takes
+roofline     = Kernel I (plz_bitmatch_kernel, ~98 % of a compress): its
+               binding roof is the int32 ALU pipe, so `achieved` is the
+               reference's matching work (one symbol compare per (aligned
+               position, window candidate) pair) per second
+               and `peak` the int32 lane-op rate measured in this run
+               (plzgpu_int_peak, LOP3); the HBM view of the same kernel and
+               the decode kernel's HBM roofline are reported beside it
+cpu_baseline = oracle/_ref (the reference library, Release flags) on this
+               host's cores over the stream's first container (256 MiB)
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -42,6 +49,8 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 METRIC = "compress/decompress GB/s (input bytes) + compression ratio at 1/2/4/8 B200 vs CPU ref"
+DATA = ("synthetic cuSZ-style quant codes (smooth field + halos, eb 1e-3, 3-D Lorenzo), "
+        "generated on device; c5 = 32 fields, seeds 42+k")
 
 
 def parse():
@@ -50,9 +59,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--workload", default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-mib", type=int, default=64)
+    ap.add_argument("--no-pageable", action="store_true")
     ap.add_argument("--interval", type=int, default=0,
                     help="reference arm only: override the workload's interval I")
     return ap.parse_args()
@@ -72,6 +81,17 @@ def load_peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def config_of(w, world, interval=None):
+    """The workload's config block — identical in both arms."""
+    return {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": interval or w.I,
+            "bytes": w.n_bytes, "containers": -(-w.n_bytes // (256 << 20)),
+            "chunks": -(-w.n_bytes // (w.C * w.S)),
+            "parallelism": (f"dp{world}: contiguous chunk-range shards of ONE stream "
+                            "(strong scaling), NCCL size all-gather + P2P segment gather"
+                            if world > 1 else "dp1"),
+            "l2": "inputs exceed the 126 MB L2; no flush needed"}
 
 
 class ClockSampler:
@@ -156,28 +176,37 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- reference arm
-def cpu_reference(workload, steps, warmup, sample_mib, quiet=False, interval=None):
-    """The reference library (oracle/_ref, compiled from its own sources) on all
-    host cores over a bounded prefix of the workload; returns GB/s figures."""
+def first_container(w, device):
+    """The stream's first container — a whole-container prefix of the very
+    bytes the B200 arm compresses: c5's field 0 (seed 42), else the first
+    256 MiB (the default block_bytes) of the workload."""
+    from paper_2304_07342_b200 import datagen
+
+    if w.fields > 1:
+        return datagen.quant_codes(w, 42, device, fields=(0, 1))
+    d = datagen.quant_codes(w, 42, device)
+    return d[: min(d.numel(), 256 << 20)].clone()
+
+
+def cpu_reference(w, steps, warmup, interval=None):
+    """The reference library (oracle/_ref: its own sources, Release flags) on
+    every host core over the stream's first container."""
     import numpy as np
     import torch
 
     import oracle as O
-    from paper_2304_07342_b200 import datagen
 
-    w = datagen.WORKLOADS[workload]
-    data = datagen.quant_codes(w, 42, "cuda" if torch.cuda.is_available() else "cpu")
-    n = min(data.numel(), sample_mib << 20)
-    host = np.ascontiguousarray(data[:n].cpu().numpy())
-    del data
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    host = np.ascontiguousarray(first_container(w, dev).cpu().numpy())
+    n = host.size
     cores = os.cpu_count() or 1
     p = O.make_params(w.S, w.W, w.C, interval or w.I)
     kind = "reference" if O.ref_available() else "port"
     ptr = host.ctypes.data
     if kind == "reference":
-        comp = lambda: O.ref_compress_into(ptr, n, p, cores)
+        comp = lambda: O.ref_compress_into(ptr, n, p, cores)  # noqa: E731
     else:
-        comp = lambda: len(O.compress(host.tobytes(), p))
+        comp = lambda: len(O.compress(host.tobytes(), p))  # noqa: E731
         cores = 1
     for _ in range(warmup):
         img_len = comp()
@@ -186,7 +215,6 @@ def cpu_reference(workload, steps, warmup, sample_mib, quiet=False, interval=Non
         t0 = time.perf_counter()
         img_len = comp()
         t.append(time.perf_counter() - t0)
-    c_gbs = n / min(t) / 1e9
     img = O.ref_compress(host.tobytes(), p, cores) if kind == "reference" else O.compress(host.tobytes(), p)
     buf = np.frombuffer(img, dtype=np.uint8).copy()
     d = []
@@ -197,9 +225,12 @@ def cpu_reference(workload, steps, warmup, sample_mib, quiet=False, interval=Non
         else:
             O.decompress(img)
         d.append(time.perf_counter() - t0)
-    return {"compress_gbs": c_gbs, "decompress_gbs": n / min(d) / 1e9, "ratio": n / img_len,
-            "cores": cores, "kind": kind, "sample_bytes": n, "workload": w.name,
-            "sample": f"first {n >> 20} MiB of {w.name} (seed 42), best of {steps}"}
+    return {"compress_gbs": n * len(t) / sum(t) / 1e9, "decompress_gbs": n * len(d) / sum(d) / 1e9,
+            "ratio": n / img_len, "cores": cores, "kind": kind, "sample_bytes": n,
+            "ms_per_step": 1e3 * sum(t) / len(t),
+            "sample": (f"the stream's first container: {n >> 20} MiB of {w.name} "
+                       f"({'field 0, ' if w.fields > 1 else ''}seed 42), mean of {len(t)} "
+                       f"compress calls after {warmup} warm-up")}
 
 
 def run_reference_arm(args):
@@ -210,36 +241,63 @@ def run_reference_arm(args):
 
     w = datagen.WORKLOADS[args.workload]
     try:
-        r = cpu_reference(args.workload, max(1, args.steps), max(0, min(args.warmup, 1)),
-                          args.cpu_sample_mib, interval=args.interval or None)
+        r = cpu_reference(w, max(1, args.steps), max(0, args.warmup), interval=args.interval or None)
     except FileNotFoundError as e:
         print(json.dumps({"impl": "reference", "unavailable": str(e)}))
         return 0
     line = {
         "metric": METRIC, "value": r["compress_gbs"], "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["sample_bytes"] / r["compress_gbs"] / 1e6,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": f"u{8 * w.S}",
-        "data": "synthetic cuSZ-style quant codes (seed 42)", "impl": "reference",
-        "config": {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": args.interval or w.I,
-                   "bytes_per_step": r["sample_bytes"], "parallelism": "host threads"},
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": f"u{8 * w.S}",
+        "data": DATA, "impl": "reference",
+        "config": config_of(w, args.gpus, args.interval or None),
         "ratio": r["ratio"],
         "decompress": {"value": r["decompress_gbs"], "unit": "GB/s"},
         "cpu_baseline": {"value": r["compress_gbs"], "unit": "GB/s", "cores": r["cores"],
-                         "kind": r["kind"], "sample": r["sample"]},
+                         "kind": r["kind"], "sample": r["sample"],
+                         "sample_bytes": r["sample_bytes"], "decompress_gbs": r["decompress_gbs"],
+                         "ratio_on_sample": r["ratio"]},
         "e2e": {"value": r["compress_gbs"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------- B200 arm
+def local_slice(w, params, rank, world, dev):
+    """This rank's contiguous chunk range of the workload stream, generated
+    on its own GPU (only the fields it overlaps); the final range also
+    returns the stream's raw tail (< S bytes)."""
+    from paper_2304_07342_b200 import datagen
+    from paper_2304_07342_b200 import dist as D
+
+    n_total = w.n_bytes
+    n_chunks, _ = D.geometry(n_total, params)
+    cb, ce = D.chunk_ranges(n_chunks, world)[rank]
+    lo = cb * w.C * w.S
+    hi = n_total if ce == n_chunks else ce * w.C * w.S
+    if w.fields > 1:
+        fb = w.field_bytes
+        k0, k1 = lo // fb, -(-hi // fb)
+        d = datagen.quant_codes(w, 42, dev, fields=(k0, k1))
+        d_local = d[lo - k0 * fb:hi - k0 * fb]
+        if d_local.numel() != d.numel():
+            d_local = d_local.clone()
+    else:
+        d = datagen.quant_codes(w, 42, dev)
+        d_local = d[lo:hi].clone() if world > 1 else d
+    tl = n_total % w.S if ce == n_chunks else 0
+    tail = bytes(d_local[d_local.numel() - tl:].cpu().tolist()) if tl else b""
+    return d_local, (cb, ce), tail, n_chunks
+
+
 def run_b200(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
-    from paper_2304_07342_b200 import datagen, plz
+    from paper_2304_07342_b200 import _lib, datagen, plz
+    from paper_2304_07342_b200 import dist as D
 
     rank, world, local = dist_env()
     gloo = os.environ.get("BENCH_DIST_BACKEND", "nccl") == "gloo"
@@ -251,205 +309,185 @@ def run_b200(args):
         if gloo:
             dist.init_process_group("gloo")
         else:
+            # the rank count is visible in NCCL's init log (driver check)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
     w = datagen.WORKLOADS[args.workload]
     params = plz.validate(plz.Params(w.S, w.W, w.C, w.I))
     ctx = plz.context(local)
-    gpu_index = local
     stream = torch.cuda.Stream(dev)
     sh = stream.cuda_stream
-
-    d_in = datagen.quant_codes(w, 42 + rank, dev)
+    n_total = w.n_bytes
+    d_in, (cb, ce), tail, n_chunks = local_slice(w, params, rank, world, dev)
     n = d_in.numel()
-    cap = plz.compress_bound(n, params)
-    img = torch.empty(cap, dtype=torch.uint8, device=dev)
-    lens = torch.zeros(4, dtype=torch.int64, device=dev)
-    out = torch.empty(n + 16, dtype=torch.uint8, device=dev)
+    cpb = (256 << 20) // (w.C * w.S)
+    aligned = cb % cpb == 0 and (ce % cpb == 0 or ce == n_chunks)
     torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    cdev = "cpu" if gloo else dev
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
+    def reduce(x: float, op) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if gloo else dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], dtype=torch.float64, device=cdev)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    # ---- compress (device-resident)
-    def compress_step():
+    def timed(fn, steps):
+        """CUDA-event ms per step on `stream`, barrier + sync both sides, max over ranks."""
+        barrier()
         with torch.cuda.stream(stream):
-            ctx.compress_async(params, d_in.data_ptr(), n, img.data_ptr(), cap, lens.data_ptr(), sh)
-
-    for _ in range(args.warmup):
-        compress_step()
-    ctx.finish(sh)
-    ptr_tok, lit_tok = ctx.finish(sh)
-    n_img = int(lens[0].item())
-    launches = ctx.last_launches
-    barrier()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        for _ in range(args.steps):
-            compress_step()
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    c_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-    ctx.finish(sh)
-
-    # ---- Kernel I alone: the roofline numerator (events around one launch
-    # of each kernel are not separable inside compress_async, so time the
-    # encode share by a second pass with the scan/assemble skipped)
-    enc_ms = encode_kernel_ms(ctx, params, d_in, n, img, cap, lens, stream, args.steps)
-
-    # ---- decompress (device-resident)
-    def decompress_step():
-        ctx.decompress_async(img.data_ptr(), n_img, out.data_ptr(), out.numel(), lens.data_ptr() + 8, sh)
-
-    for _ in range(args.warmup):
-        decompress_step()
-    ctx.finish(sh)
-    barrier()
-    ev[0].record(stream)
-    for _ in range(args.steps):
-        decompress_step()
-    ev[1].record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    d_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-    ctx.finish(sh)
-    roundtrip_ok = bool(torch.equal(out[:n], d_in))
-
-    # ---- N > 1: the sharded stream — rank r holds chunk range
-    # r of the global input (the union of the ranks' fields), NCCL all-gathers
-    # per-container sizes, rank 0 receives every rank's segments into one
-    # image.  This is the multi-GPU step that is timed for `value`.
-    shard = None
-    if world > 1:
-        from paper_2304_07342_b200 import dist as D
-
-        n_total = n * world
-        n_chunks, _ = D.geometry(n_total, params)
-        cb, ce = D.chunk_ranges(n_chunks, world)[rank]
-        lo = cb * w.C * w.S
-        hi = n_total if ce == n_chunks else ce * w.C * w.S
-        shard_in = d_in.repeat((hi - lo + n - 1) // n)[: hi - lo].contiguous()
-        tail = bytes(shard_in[shard_in.numel() - n_total % w.S:].cpu().tolist()) if (
-            ce == n_chunks and n_total % w.S) else b""
-        backend = D.GpuBackend(params, gpu_index, ctx)
-        comm = D.TorchComm("cpu" if gloo else dev)
-
-        def shard_step():
-            with torch.cuda.stream(stream):
-                return D.compress_sharded(backend, comm, params, n_total, shard_in, tail, sh)
-
-        for _ in range(args.warmup):
-            shard_step()
-        barrier()
-        ev[0].record(stream)
-        for _ in range(args.steps):
-            img_s, img_len_s = shard_step()
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        s_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-        shard = {"ms_per_step": s_ms, "image_bytes": img_len_s, "input_bytes": n_total,
-                 "ratio": n_total / img_len_s, "chunk_range": [cb, ce]}
-        back = None
-        if rank == 0:  # the gathered stream decodes to the union of the shards
-            back = plz.decompress_bytes(img_s[:img_len_s])
-            shard["roundtrip_ok"] = bool(back.numel() == n_total)
-        del shard_in
-
-        # sharded decompress of that stream (every rank holds the image, rank
-        # r decodes chunk range r: dist.decompress_sharded, no gather timed)
-        cdev = "cpu" if gloo else dev
-        ln_t = torch.tensor([img_len_s if rank == 0 else 0], dtype=torch.int64, device=cdev)
-        dist.broadcast(ln_t, 0)
-        L_img = int(ln_t.item())
-        if rank == 0:
-            img_full = img_s[:L_img].contiguous()
-        else:
-            img_full = torch.empty(L_img, dtype=torch.uint8, device=dev)
-        if gloo:
-            buf = img_full.cpu()
-            dist.broadcast(buf, 0)
-            img_full = buf.to(dev)
-        else:
-            dist.broadcast(img_full, 0)
-
-        def dec_shard_step(gather=False):
-            with torch.cuda.stream(stream):
-                return D.decompress_sharded(backend, comm, img_full, gather, sh)
-
-        for _ in range(args.warmup):
-            dec_shard_step()
-        barrier()
-        ev[0].record(stream)
-        for _ in range(args.steps):
-            dec_shard_step()
-        ev[1].record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        sd_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-        whole, _, _ = dec_shard_step(True)
-        shard["decompress"] = {"value": n_total / (sd_ms * 1e-3) / 1e9, "unit": "GB/s",
-                               "ms_per_step": sd_ms,
-                               "note": "dist.decompress_sharded: rank r decodes chunk range r "
-                                       "of the one image (plzgpu_decompress_range), no gather"}
-        if rank == 0:
-            shard["decompress"]["roundtrip_ok"] = bool(torch.equal(whole.to(back.device), back))
-        del img_full, whole
-
-    # ---- end to end through the public call with host buffers
-    h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    h_in.copy_(d_in)
-    h_img = torch.empty(cap, dtype=torch.uint8, pin_memory=True)
-    h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-
-    def e2e_compress():
-        return ctx.compress_ptr(params, h_in.data_ptr(), n, h_img.data_ptr(), cap, sh)[0]
-
-    def e2e_decompress():
-        return ctx.decompress_ptr(h_img.data_ptr(), n_img, h_out.data_ptr(), n, sh)
-
-    for _ in range(max(1, args.warmup)):
-        e2e_compress()
-        e2e_decompress()
-    barrier()
-    ev[0].record(stream)
-    for _ in range(args.steps):
-        e2e_compress()
-    ev[1].record(stream)
-    torch.cuda.synchronize()
-    e2e_c_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-    h_out.zero_()
-    barrier()
-    ev[0].record(stream)
-    for _ in range(args.steps):
-        e2e_decompress()
-    ev[1].record(stream)
-    torch.cuda.synchronize()
-    e2e_d_ms = max_over_ranks(ev[0].elapsed_time(ev[1]) / args.steps)
-    e2e_ok = bytes(h_img[:n_img].numpy().tobytes()) == bytes(img[:n_img].cpu().numpy().tobytes())
-    e2e_dec_ok = bool(torch.equal(h_out, h_in))
-    # the link's own ceiling: plain pinned copies of the same n bytes
-    link = {}
-    for name, fn in (("h2d_gbs", lambda: d_in.copy_(h_in, non_blocking=True)),
-                     ("d2h_gbs", lambda: h_out.copy_(d_in, non_blocking=True))):
-        with torch.cuda.stream(stream):
-            fn()
             ev[0].record(stream)
-            for _ in range(3):
+            for _ in range(steps):
                 fn()
             ev[1].record(stream)
         torch.cuda.synchronize()
-        link[name] = n * 3 / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9
+        barrier()
+        return reduce(ev[0].elapsed_time(ev[1]) / steps, dist.ReduceOp.MAX if world > 1 else None)
+
+    # ---- compress (device-resident): one image of the whole stream
+    if world == 1:
+        cap = plz.compress_bound(n, params)
+        img = torch.empty(cap, dtype=torch.uint8, device=dev)
+        lens = torch.zeros(4, dtype=torch.int64, device=dev)
+
+        def compress_step():
+            ctx.compress_async(params, d_in.data_ptr(), n, img.data_ptr(), cap, lens.data_ptr(), sh)
+    else:
+        backend = D.GpuBackend(params, local, ctx)
+        comm = D.TorchComm(cdev)
+        shard_out = {}
+
+        def compress_step():
+            shard_out["img"], shard_out["len"] = D.compress_sharded(backend, comm, params, n_total,
+                                                                    d_in, tail, sh)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            compress_step()
+    torch.cuda.synchronize()
+    if world == 1:
+        ptr_tok, lit_tok = ctx.finish(sh)
+        img_len = int(lens[0].item())
+        launches_per_step = ctx.last_launches
+    else:
+        img_len = int(reduce(float(shard_out["len"]), dist.ReduceOp.MAX))
+        ctx.shard_encode(params, d_in.data_ptr(), n_total, cb, ce, sh)  # its launch count
+        launches_per_step = ctx.last_launches + 1 + (1 if rank == 0 else 0)
+        st = ctx.finish(sh)
+        ptr_tok = int(reduce(float(st[0]), dist.ReduceOp.SUM))
+        lit_tok = int(reduce(float(st[1]), dist.ReduceOp.SUM))
+    with ClockSampler(local) as clk:
+        c_ms = timed(compress_step, args.steps)
+
+    # ---- Kernel I alone (the roofline numerator) on this rank's bytes
+    enc_ms = reduce(encode_kernel_ms(ctx, params, d_in, n, stream, args.steps),
+                    dist.ReduceOp.MAX if world > 1 else None)
+
+    # ---- decompress (device-resident)
+    if world == 1:
+        out = torch.empty(n + 16, dtype=torch.uint8, device=dev)
+        ctx_img = img
+
+        def decompress_step():
+            ctx.decompress_async(img.data_ptr(), img_len, out.data_ptr(), out.numel(),
+                                 lens.data_ptr() + 8, sh)
+    else:
+        # every rank holds the one image; rank r decodes chunk range r
+        if rank == 0:
+            ctx_img = shard_out["img"][:img_len].contiguous()
+        else:
+            ctx_img = torch.empty(img_len, dtype=torch.uint8, device=dev)
+        if gloo:
+            buf = ctx_img.cpu()
+            dist.broadcast(buf, 0)
+            ctx_img = buf.to(dev)
+        else:
+            dist.broadcast(ctx_img, 0)
+        shard_out.clear()
+        dec = {}
+
+        def decompress_step():
+            dec["r"] = D.decompress_sharded(backend, comm, ctx_img, False, sh)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            decompress_step()
+    if world == 1:
+        ctx.finish(sh)
+    d_ms = timed(decompress_step, args.steps)
+    if world == 1:
+        ctx.finish(sh)
+        roundtrip_ok = bool(torch.equal(out[:n], d_in))
+    else:
+        _, dslice, dbegin = dec["r"]
+        roundtrip_ok = bool(torch.equal(dslice, d_in)) and dbegin == cb * w.C * w.S
+        roundtrip_ok = bool(reduce(float(roundtrip_ok), dist.ReduceOp.MIN))
+        del dec
+    del ctx_img
+    if world == 1:
+        del out
+
+    # ---- end to end through the public call with pinned HOST buffers: at
+    # N>1 each rank compresses its host shard — whole containers when the
+    # ranges align with them (c5 at 1/2/4/8), so the parts concatenate to
+    # the one image
+    e2e = None
+    if world == 1 or aligned:
+        h_in = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        h_in.copy_(d_in)
+        hcap = plz.compress_bound(n, params)
+        h_img = torch.empty(hcap, dtype=torch.uint8, pin_memory=True)
+        h_out = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+        part = {}
+
+        def e2e_compress():
+            part["len"] = ctx.compress_ptr(params, h_in.data_ptr(), n, h_img.data_ptr(), hcap, sh)[0]
+
+        def e2e_decompress():
+            ctx.decompress_ptr(h_img.data_ptr(), part["len"], h_out.data_ptr(), n, sh)
+
+        for _ in range(max(1, args.warmup)):
+            e2e_compress()
+            e2e_decompress()
+        e2e_c_ms = timed(e2e_compress, args.steps)
+        h_out.zero_()
+        e2e_d_ms = timed(e2e_decompress, args.steps)
+        part_len = part["len"]
+        e2e_dec_ok = bool(reduce(float(torch.equal(h_out, h_in)), dist.ReduceOp.MIN if world > 1 else None))
+        if world == 1:
+            same = bool(torch.equal(h_img[:part_len].to(dev), img[:img_len]))
+        else:
+            same = int(reduce(float(part_len), dist.ReduceOp.SUM)) == img_len
+        # the link's own ceiling: plain pinned copies of the same n bytes
+        link = {}
+        for name, fn in (("h2d_gbs", lambda: d_in.copy_(h_in, non_blocking=True)),
+                         ("d2h_gbs", lambda: h_out.copy_(d_in, non_blocking=True))):
+            link[name] = n_total / (timed(fn, 3) * 1e-3) / 1e9
+        e2e = {"value": n_total / (e2e_c_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": n_total, "d2h_bytes_per_step": img_len,
+               "matches_device_image": same,
+               "decompress": {"value": n_total / (e2e_d_ms * 1e-3) / 1e9, "unit": "GB/s",
+                              "h2d_bytes_per_step": img_len, "d2h_bytes_per_step": n_total,
+                              "roundtrip_ok": e2e_dec_ok},
+               "link": {**link, "note": "plain pinned cudaMemcpy of the same bytes: "
+                                        "the PCIe ceiling e2e runs against"},
+               "api": "plzgpu_compress / plzgpu_decompress (C-ABI) with pinned host buffers"
+                      + ("; one call per rank on its host shard of whole containers" if world > 1 else "")}
+        del h_in, h_img, h_out
+        # pageable buffers (the std::vector path of plz::compress callers)
+        if world == 1 and not args.no_pageable:
+            e2e["pageable"] = pageable_e2e(ctx, params, d_in, n, img_len, stream, sh, timed,
+                                           max(1, min(args.steps, 3)))
+    else:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "rank ranges do not align with containers at this N"}
 
     if rank != 0:
         if world > 1:
@@ -457,88 +495,118 @@ def run_b200(args):
             dist.destroy_process_group()
         return 0
 
-    total_in = n * world
+    # ---- rooflines
     peak, peak_kind = load_peaks()
-    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
-    int_peak = torch.cuda.get_device_properties(dev).multi_processor_count * 128 * sm_mhz * 1e6
-    prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {[1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]}, 16>")
-    enc_bytes = n + n_img  # input read + staged tokens written (~ image)
-    achieved = enc_bytes / (enc_ms * 1e-3) / 1e9
+    int_peaks = {}
+    for op, name in ((0, "lop3"), (1, "iadd3"), (2, "shf"), (3, "popc_iadd")):
+        v, e = ctypes.c_double(), _lib.Error()
+        if _lib.lib().plzgpu_int_peak(local, op, ctypes.byref(v), ctypes.byref(e)) == 0:
+            int_peaks[name] = v.value
+    nw = [1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]
+    prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {nw}, 16>")
+    dprof = ncu_profile_facts("plz_decode_kernel")
+    pairs = match_pairs(n, w)
+    pairs_s = pairs / (enc_ms * 1e-3)
+    lane_peak = int_peaks.get("lop3")
+    enc_bytes = n + img_len / world  # input read + staged tokens written (~ image share)
+    dec_bytes = img_len + n_total    # image read + output written
+    dec_gbs = dec_bytes / (d_ms * 1e-3) / 1e9
     line = {
         "metric": METRIC,
-        "value": total_in / (c_ms * 1e-3) / 1e9,
+        "value": n_total / (c_ms * 1e-3) / 1e9,
         "unit": "GB/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": c_ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": f"u{8 * w.S}",
-        "data": "synthetic cuSZ-style quant codes (smooth field + halos, eb 1e-3, 3-D Lorenzo), "
-                "generated on device, seed 42+rank",
-        "config": {"workload": w.name, "S": w.S, "W": w.W, "C": w.C, "I": w.I,
-                   "bytes_per_rank": n, "chunks_per_rank": -(-n // (w.C * w.S)),
-                   "parallelism": (f"dp{world}: chunk-range shards of one stream, NCCL size "
-                                   "all-gather + P2P segment gather" if world > 1 else "dp1"),
-                   "l2": "inputs (337 MB) exceed the 126 MB L2; no flush needed"},
-        "ratio": n / n_img,
-        "decompress": {"value": total_in / (d_ms * 1e-3) / 1e9, "unit": "GB/s",
+        "data": DATA,
+        "config": config_of(w, world),
+        "ratio": n_total / img_len,
+        "image_bytes": img_len,
+        "decompress": {"value": n_total / (d_ms * 1e-3) / 1e9, "unit": "GB/s",
                        "ms_per_step": d_ms, "roundtrip_ok": roundtrip_ok},
-        "e2e": {"value": total_in / (e2e_c_ms * 1e-3) / 1e9, "unit": "GB/s",
-                "h2d_bytes_per_step": n, "d2h_bytes_per_step": n_img,
-                "matches_device_image": e2e_ok,
-                "decompress": {"value": total_in / (e2e_d_ms * 1e-3) / 1e9, "unit": "GB/s",
-                               "h2d_bytes_per_step": n_img, "d2h_bytes_per_step": n,
-                               "roundtrip_ok": e2e_dec_ok},
-                "link": {**link, "note": "plain pinned cudaMemcpy of the same bytes: "
-                                         "the PCIe ceiling e2e runs against"}},
-        "roofline": {"kernel": "plz_bitmatch_kernel (Kernel I, bitmap pass)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_kind": peak_kind,
-                     "traffic": prof["dram_bytes"] if prof else None,
-                     "bytes_per_launch": enc_bytes, "ms_per_launch": enc_ms,
-                     "note": "Kernel I is integer-ALU bound, not HBM bound: the ALU-pipe "
-                             "utilisation below is its binding roofline (ncu, profiles/)",
-                     "alu_pipe": ({"frac": prof["alu_pipe_pct"] / 100, "issue_active":
-                                   prof["issue_active_pct"] / 100, "source": prof["source"]}
-                                  if prof and prof.get("alu_pipe_pct") else None),
-                     # SURVEY.md §8d's matching unit: one symbol compare per
-                     # (aligned position, window candidate) — the reference
-                     # matcher's work, which Kernel I's bitmaps replace with
-                     # W/32 word operations per step
-                     "match_pairs": {"pairs_per_launch": match_pairs(n, w),
-                                     "pairs_per_s": match_pairs(n, w) / (enc_ms * 1e-3),
-                                     # SURVEY.md §8d's int_fraction: pairs/s over the
-                                     # int32 lane-op peak (148 SMs x 128 lanes x clock);
-                                     # > 1 would be possible — a bitmap word op covers
-                                     # 32 pairs
-                                     "int_peak_ops_per_s": int_peak,
-                                     "int_fraction": match_pairs(n, w) / (enc_ms * 1e-3) / int_peak}},
+        "e2e": e2e,
+        "roofline": {
+            "kernel": f"plz_bitmatch_kernel<{w.S},{nw},16> (Kernel I: match + greedy walk + encode)",
+            "bound": "int32-alu",
+            "achieved": pairs_s / 1e9,
+            "peak": lane_peak / 1e9 if lane_peak else None,
+            "unit": "G pair-compares/s vs G int32 lane-ops/s",
+            "frac": pairs_s / lane_peak if lane_peak else None,
+            "traffic": prof["dram_bytes"] if prof else None,
+            "peak_kind": "measured in this run (plzgpu_int_peak: LOP3 lane-ops/s)",
+            "pairs_per_launch": pairs, "ms_per_launch": enc_ms,
+            "note": ("achieved = the reference matcher's work (one symbol compare per aligned "
+                     "position x window candidate, SURVEY.md §8d) per second; Kernel I does it "
+                     "with W/32 bitmap word-ops per step, so frac may exceed 1"),
+            "int_peaks_lane_ops_per_s": int_peaks,
+            "alu_pipe": ({"frac": prof["alu_pipe_pct"] / 100,
+                          "issue_active": prof["issue_active_pct"] / 100,
+                          "source": prof["source"]} if prof and prof.get("alu_pipe_pct") else None),
+            "hbm": {"achieved": enc_bytes / (enc_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": enc_bytes / (enc_ms * 1e-3) / 1e9 / peak, "peak_kind": peak_kind,
+                    "bytes_per_launch": enc_bytes},
+        },
+        "roofline_decompress": {
+            "kernel": "plz_parse_kernel + plz_decode_kernel (decode ~98 % of the step)",
+            "bound": "hbm", "achieved": dec_gbs, "peak": peak, "unit": "GB/s",
+            "frac": dec_gbs / peak, "peak_kind": peak_kind, "bytes_per_step": dec_bytes,
+            "traffic": dprof["dram_bytes"] if dprof else None,
+            "source": dprof["source"] if dprof else None},
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
-        "gpu_launches": (launches if world == 1 else 4) * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
-    if shard is not None:
-        # whole-job value = the sharded multi-GPU compress of the union
-        line["value"] = shard["input_bytes"] / (shard["ms_per_step"] * 1e-3) / 1e9
-        line["ms_per_step"] = shard["ms_per_step"]
-        line["sharded_stream"] = shard
-        line["per_rank_independent_compress_gbs"] = total_in / (c_ms * 1e-3) / 1e9
-    if not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference(args.workload, 2, 0, args.cpu_sample_mib)
+            r = cpu_reference(w, 2, 0)
             line["cpu_baseline"] = {"value": r["compress_gbs"], "unit": "GB/s", "cores": r["cores"],
                                     "kind": r["kind"], "sample": r["sample"],
-                                    "decompress_gbs": r["decompress_gbs"], "ratio": r["ratio"]}
+                                    "sample_bytes": r["sample_bytes"],
+                                    "decompress_gbs": r["decompress_gbs"],
+                                    "ratio_on_sample": r["ratio"]}
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"unavailable": str(e)}
-    print(json.dumps(line))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
     return 0
+
+
+def pageable_e2e(ctx, params, d_in, n, img_len, stream, sh, timed, steps):
+    """e2e through plzgpu_compress / plzgpu_decompress with pageable host
+    buffers (what plz::compress(std::span) / std::vector callers pass)."""
+    import torch
+
+    from paper_2304_07342_b200 import plz
+
+    cap = plz.compress_bound(n, params)
+    p_in = torch.empty(n, dtype=torch.uint8)
+    p_in.copy_(d_in)
+    p_img = torch.empty(cap, dtype=torch.uint8)
+    p_out = torch.empty(n, dtype=torch.uint8)
+    part = {}
+
+    def comp():
+        part["len"] = ctx.compress_ptr(params, p_in.data_ptr(), n, p_img.data_ptr(), cap, sh)[0]
+
+    def decomp():
+        ctx.decompress_ptr(p_img.data_ptr(), part["len"], p_out.data_ptr(), n, sh)
+
+    comp()
+    decomp()
+    c_ms = timed(comp, steps)
+    p_out.zero_()
+    d_ms = timed(decomp, steps)
+    ok = part["len"] == img_len and bool(torch.equal(p_out, p_in))
+    return {"value": n / (c_ms * 1e-3) / 1e9, "unit": "GB/s",
+            "decompress": n / (d_ms * 1e-3) / 1e9, "steps": steps, "roundtrip_ok": ok,
+            "h2d_bytes_per_step": n, "d2h_bytes_per_step": img_len}
 
 
 def match_pairs(n_bytes: int, w) -> int:
@@ -556,8 +624,8 @@ def match_pairs(n_bytes: int, w) -> int:
 
 def ncu_profile_facts(kernel: str):
     """DRAM traffic per launch and pipe utilisation of `kernel` from the newest
-    committed ncu capture (profiles/<round>/kernel_metrics.csv) — measured by
-    tools/profile_round.sh on a B200, not inside this run."""
+    committed ncu capture of this code (profiles/<round>/kernel_metrics.csv,
+    tools/profile_round.sh on a B200) — not measured inside this run."""
     import csv
     import glob
 
@@ -576,11 +644,9 @@ def ncu_profile_facts(kernel: str):
             "issue_active_pct": f("issue_active_pct"), "sm_throughput_pct": f("sm_throughput_pct")}
 
 
-def encode_kernel_ms(ctx, params, d_in, n, img, cap, lens, stream, steps):
+def encode_kernel_ms(ctx, params, d_in, n, stream, steps):
     """CUDA-event time of Kernel I alone via the library's encode-only entry."""
     import torch
-
-    from paper_2304_07342_b200 import plz
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     sh = stream.cuda_stream
@@ -591,7 +657,6 @@ def encode_kernel_ms(ctx, params, d_in, n, img, cap, lens, stream, steps):
         ctx.encode_only(params, d_in.data_ptr(), n, sh)
     ev[1].record(stream)
     torch.cuda.synchronize()
-    del plz
     return ev[0].elapsed_time(ev[1]) / steps
 
 

@@ -166,19 +166,27 @@ int plzgpu_decompress_range(plzgpu_ctx* ctx, const void* img, uint64_t len, uint
 
 /* One stream compressed by several GPUs of this process (SURVEY.md §8b item
  * 4: "a multi-GPU variant taking a device list"): chunk ranges encoded
- * concurrently (one context and host thread per entry of `devices`; an entry
- * may repeat a device), segments gathered into one image on devices[0] by
- * peer copies, then copied to `out` (host or device).  The image equals
- * plzgpu_compress's.  Replaces plz::compress (pipeline.hpp:28-30) for a
- * device list; the one-process-per-GPU form is dist.compress_sharded. */
+ * concurrently (one pooled context and host thread per entry of `devices`;
+ * an entry may repeat a device), each rank's Kernel III writing its segments
+ * straight into the image on devices[0] through peer access (NVLink), the
+ * headers written there, then the image to `out` (host or device; a device
+ * `out` on devices[0] is written in place).  The image equals
+ * plzgpu_compress's.  Contexts and scratch persist across calls (per device,
+ * process-wide pool); the caller's current device is preserved.  A device
+ * `in` must be complete when the call starts (the ranks run on their own
+ * streams): synchronize the stream that wrote it first.  Replaces
+ * plz::compress (pipeline.hpp:28-30) for a device list; the
+ * one-process-per-GPU form is dist.compress_sharded. */
 int plzgpu_compress_multi(const int* devices, int n_devices, const plzgpu_params* params,
                           const void* in, uint64_t n, void* out, uint64_t cap, uint64_t* out_len,
                           plzgpu_stats* stats, plzgpu_error* err);
 
 /* One image decompressed by several GPUs of this process: rank r decodes the
- * global chunk range r (plzgpu_decompress_range) on devices[r] and its slice
- * lands at its offset in `out` (host or device).  Output and errors equal
- * plzgpu_decompress's. */
+ * global chunk range r (plzgpu_decompress_range) on devices[r]; with a
+ * device `out` its slice is decoded straight into `out` at its offset
+ * (peer stores), with a host `out` it is copied there from rank r's GPU.
+ * Output and errors equal plzgpu_decompress's.  Same pooling, device and
+ * ordering rules as plzgpu_compress_multi. */
 int plzgpu_decompress_multi(const int* devices, int n_devices, const void* img, uint64_t len,
                             void* out, uint64_t cap, uint64_t* out_len, plzgpu_error* err);
 
@@ -238,6 +246,13 @@ int plzgpu_shard_assemble(plzgpu_ctx* ctx, const uint64_t* bases, void* d_out, u
                           uint64_t* segs, uint64_t max_segs, uint64_t* n_segs, uint64_t* out_len,
                           void* stream, plzgpu_error* err);
 
+/* The same segments written straight to their offsets in the final image
+ * d_img (img_cap bytes; device memory of this context's GPU or, with peer
+ * access enabled, of another GPU: Kernel III then stores over NVLink and
+ * nothing is gathered afterwards). */
+int plzgpu_shard_assemble_into(plzgpu_ctx* ctx, const uint64_t* bases, void* d_img,
+                               uint64_t img_cap, void* stream, plzgpu_error* err);
+
 /* Root: write every container's header, final table entries and tail into
  * d_img given per-container {payload total, flag total} for ALL containers and
  * the input's last tail_len (< S) bytes (host).  *img_len = image length. */
@@ -270,6 +285,12 @@ int plzgpu_pointer_histogram(plzgpu_ctx* ctx, const plzgpu_params* params, const
  * produced. */
 int plzgpu_profile_encode(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
                           uint64_t n, void* stream, plzgpu_error* err);
+
+/* Measured int32 lane-op throughput of `device` (lane operations per
+ * second): op 0 = LOP3, 1 = IADD, 2 = SHF (funnel shift), 3 = POPC + IADD.
+ * The denominator of the matching kernel's integer roofline (SURVEY.md
+ * §8d); runs two short launches on the device's legacy stream. */
+int plzgpu_int_peak(int device, int op, double* lane_ops_per_s, plzgpu_error* err);
 
 /* ---------------------------------- cuSZ dual quantization (use case) */
 

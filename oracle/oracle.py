@@ -78,6 +78,14 @@ def make_params(S=2, W=128, C_=2048, I=1, block_bytes=256 << 20, min_match=None)
 
 
 def _buf(data) -> tuple:
+    try:  # contiguous numpy bytes: passed in place (no copy of GiB-sized inputs)
+        import numpy as np
+
+        if isinstance(data, np.ndarray) and data.dtype == np.uint8 and data.flags["C_CONTIGUOUS"] \
+                and data.size:
+            return C.cast(data.ctypes.data, C.c_char_p), data.size, data
+    except ImportError:
+        pass
     b = bytes(data)
     return C.c_char_p(b) if b else C.c_char_p(b"\0"), len(b), b
 

@@ -18,6 +18,7 @@
 #include "plz/format.hpp"
 #include "plz/matcher.hpp"
 #include "plz/params.hpp"
+#include "plz/partition.hpp"
 #include "plz/pipeline.hpp"
 #include "plz_oracle.h"
 
@@ -98,6 +99,36 @@ int plzref_compress(const unsigned char* in, std::uint64_t n, const plzo_params*
         plz::PipelineStats st;
         const auto img =
             plz::compress(std::span<const std::uint8_t>(in, n), to_params(p), threads, &st);
+        *out = dup(img);
+        *out_len = img.size();
+        if (stats) {
+            stats[0] = st.max_cmp_per_pos;
+            stats[1] = st.pointer_tokens;
+            stats[2] = st.literal_tokens;
+        }
+    });
+}
+
+// plzref::compress_block (pipeline.cpp:26-86) for one block of a plan,
+// serialised with plzref::write_container (format.cpp:75-104).
+int plzref_compress_block(const unsigned char* block, std::uint64_t n, std::uint64_t byte_start,
+                          std::uint64_t byte_len, std::uint32_t num_chunks,
+                          std::uint32_t last_chunk_len, std::uint8_t tail_len,
+                          const plzo_params* p, int threads, unsigned char** out,
+                          std::uint64_t* out_len, std::uint64_t* stats, plzo_error* err) {
+    *out = nullptr;
+    *out_len = 0;
+    return guarded(err, [&] {
+        plz::BlockPlan bp;
+        bp.byte_start = byte_start;
+        bp.byte_len = byte_len;
+        bp.num_chunks = num_chunks;
+        bp.last_chunk_len = last_chunk_len;
+        bp.tail_len = tail_len;
+        plz::PipelineStats st;
+        const plz::Container c = plz::compress_block(std::span<const std::uint8_t>(block, n), bp,
+                                                     to_params(p), threads, &st);
+        const auto img = plz::write_container(c);
         *out = dup(img);
         *out_len = img.size();
         if (stats) {

@@ -80,6 +80,7 @@ SIGNATURES = [  # every entry point of include/plzgpu.h
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),
     ("plzgpu_decompress_chunk", C.c_int, [_VP, _VP, _U64, _VP, _U64, _U64, _P, _U64, _VP, _E]),
     ("plzgpu_profile_encode", C.c_int, [_VP, _P, _VP, _U64, _VP, _E]),
+    ("plzgpu_int_peak", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), _E]),
     ("plzgpu_match_table", C.c_int, [_VP, _P, _VP, _U64, _VP, _VP, C.POINTER(_U64), _VP, _E]),
     ("plzgpu_pointer_histogram", C.c_int, [_VP, _P, _VP, _U64, C.POINTER(_U64), _VP, _E]),
     ("plzgpu_num_chunks", _U64, [_U64, _P]),
@@ -90,6 +91,7 @@ SIGNATURES = [  # every entry point of include/plzgpu.h
                                      C.POINTER(_U64), _U64]),
     ("plzgpu_shard_assemble", C.c_int, [_VP, C.POINTER(_U64), _VP, _U64, C.POINTER(_U64), _U64,
                                         C.POINTER(_U64), C.POINTER(_U64), _VP, _E]),
+    ("plzgpu_shard_assemble_into", C.c_int, [_VP, C.POINTER(_U64), _VP, _U64, _VP, _E]),
     ("plzgpu_shard_headers", C.c_int, [_VP, _P, _U64, C.POINTER(_U64), _VP, _VP, _U64,
                                        C.POINTER(_U64), _VP, _E]),
     ("plzgpu_lorenzo_quantize", C.c_int, [_VP, _VP, _U64, _U64, _U64, C.c_double, C.c_int32, _VP,

@@ -30,13 +30,18 @@ class Workload:
     C: int
     I: int
     lorenzo: int        # 1 or 3 (dimensions)
+    fields: int = 1     # independent fields of `shape`, seeds seed+k, back to back
 
     @property
-    def n_bytes(self) -> int:
+    def field_bytes(self) -> int:
         n = 1
         for s in self.shape:
             n *= s
         return n * {"u8": 1, "u16": 2, "u32": 4}[self.dtype]
+
+    @property
+    def n_bytes(self) -> int:
+        return self.fields * self.field_bytes
 
 
 # BASELINE.json configs; "window 256" runs as W=255 (params.cpp:22-23), a
@@ -46,7 +51,10 @@ WORKLOADS = {
     "c2": Workload("c2-u16-cesm-26x1800x3600", (26, 1800, 3600), "u16", 512, 2, 255, 2048, 2, 3),
     "c3": Workload("c3-u16-nyx-512^3", (512, 512, 512), "u16", 512, 2, 255, 2048, 1, 3),
     "c4": Workload("c4-u32-1GiB", (256, 1024, 1024), "u32", 512, 4, 255, 1024, 4, 3),
-    "c5": Workload("c5-u16-8GiB", (32 * 512, 512, 512), "u16", 512, 2, 255, 2048, 2, 3),
+    # 8 GiB as 32 NYX-like 256 MiB fields with seeds 42+k — one
+    # 256 MiB container each at the default block size, so the stream's first
+    # container is exactly c3's field (seed 42)
+    "c5": Workload("c5-u16-8GiB", (512, 512, 512), "u16", 512, 2, 255, 2048, 2, 3, fields=32),
 }
 # Field model, in units of the quantisation step 2*eb.  With a relative error
 # bound of 1e-3 the value range spans 1 / (2 * 1e-3) = 500 steps: localised
@@ -100,12 +108,29 @@ def _field(shape, seed: int, device):
     return f
 
 
-def quant_codes(w: Workload, seed: int = 42, device=None):
-    """Return a flat torch.uint8 tensor with the workload's code bytes."""
+def quant_codes(w: Workload, seed: int = 42, device=None, fields=None):
+    """Return a flat torch.uint8 tensor with the workload's code bytes.
+
+    Multi-field workloads (c5) are the concatenation of fields k = 0..F-1,
+    field k generated from seed + k; `fields` = (first, end) selects a
+    contiguous run of them (a rank's share, or the reference arm's first
+    container) without generating the rest."""
     import torch
 
     if device is None:
         device = "cuda" if torch.cuda.is_available() else "cpu"
+    if w.fields > 1 or fields is not None:
+        k0, k1 = fields if fields is not None else (0, w.fields)
+        out = torch.empty((k1 - k0) * w.field_bytes, dtype=torch.uint8, device=device)
+        for k in range(k0, k1):
+            out[(k - k0) * w.field_bytes:(k - k0 + 1) * w.field_bytes] = _one_field(w, seed + k, device)
+        return out
+    return _one_field(w, seed, device)
+
+
+def _one_field(w: Workload, seed: int, device):
+    import torch
+
     f = _field(w.shape, seed, device)
     gen = torch.Generator(device=device).manual_seed(seed + 1000)
     f += NOISE_SIGMA * torch.randn(f.shape, generator=gen, device=device, dtype=torch.float32)

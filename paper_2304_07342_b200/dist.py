@@ -135,6 +135,10 @@ class GpuBackend:
                                                  out.data_ptr(), out.numel(), stream)
         return out[:ln], begin
 
+    def decode_all(self, img):
+        """The single-call decode of the whole image (error reporting)."""
+        return plz.decompress_bytes(img)
+
     def headers(self, n_total: int, plan: Plan, tail: bytes, img, stream: int = 0) -> int:
         return self.ctx.shard_headers(self.params, n_total, plan.totals, tail, img.data_ptr(),
                                       img.numel(), stream)
@@ -188,8 +192,28 @@ class TorchComm:
                 img[off:off + buf.numel()].copy_(buf)
 
 
-def _pack(totals: Totals, tail: bytes, max_touched: int) -> List[int]:
-    vec = [-1] * (3 * max_touched) + [len(tail)] + list(tail) + [0] * (3 - len(tail))
+_ERR_CLASSES = {L.VALIDATION: plz.ValidationError, L.UNSUPPORTED_FORMAT: plz.UnsupportedFormatError,
+                L.CORRUPTION: plz.CorruptionError, L.CONTRACT: plz.ContractError,
+                L.CAPACITY: plz.CapacityError}
+
+
+def _status_of(exc) -> int:
+    for code, cls in _ERR_CLASSES.items():
+        if type(exc) is cls:
+            return code
+    return L.CUDA
+
+
+def _raise_remote(rank: int, status: int, own):
+    """Every rank raises once any rank failed: its own error, or one of the
+    failing rank's type naming it (no rank is left waiting in a collective)."""
+    if own is not None:
+        raise own
+    raise _ERR_CLASSES.get(status, plz.CudaError)(f"rank {rank} failed (error code {status})")
+
+
+def _pack(totals: Totals, tail: bytes, max_touched: int, status: int = 0) -> List[int]:
+    vec = [-1] * (3 * max_touched) + [len(tail)] + list(tail) + [0] * (3 - len(tail)) + [status]
     for i, row in enumerate(totals):
         vec[3 * i:3 * i + 3] = list(row)
     return vec
@@ -198,7 +222,7 @@ def _pack(totals: Totals, tail: bytes, max_touched: int) -> List[int]:
 def _unpack(vec: List[int], max_touched: int):
     totals = [tuple(vec[3 * i:3 * i + 3]) for i in range(max_touched) if vec[3 * i] >= 0]
     tl = vec[3 * max_touched]
-    return totals, bytes(vec[3 * max_touched + 1:3 * max_touched + 1 + tl])
+    return totals, bytes(vec[3 * max_touched + 1:3 * max_touched + 1 + tl]), vec[-1]
 
 
 def compress_sharded(backend, comm, params: plz.Params, n_total: int, d_local,
@@ -212,11 +236,22 @@ def compress_sharded(backend, comm, params: plz.Params, n_total: int, d_local,
     rng = ranges[comm.rank]
     cpb = params.block_bytes // (params.chunk_size * params.symbol_width)
     max_touched = max((e - b + cpb - 1) // cpb + 1 for b, e in ranges)
-    mine = backend.encode(d_local, n_total, rng, stream)
-    gathered = [_unpack(v, max_touched) for v in comm.allgather(_pack(mine, tail, max_touched))]
+    own = None
+    try:
+        mine = backend.encode(d_local, n_total, rng, stream)
+    except plz.Error as e:  # reported after the exchange, on every rank
+        own, mine = e, []
+    gathered = [_unpack(v, max_touched)
+                for v in comm.allgather(_pack(mine, tail, max_touched, _status_of(own) if own else 0))]
+    for r, g in enumerate(gathered):
+        if g[2]:
+            _raise_remote(r, g[2], own if r == comm.rank else None)
     per_rank = [g[0] for g in gathered]
     tail_all = b"".join(g[1] for g in gathered)
     plan = plan_offsets(n_total, params, per_rank)
+    if any(p > 0xFFFFFFFF or f > 0xFFFFFFFF for p, f in plan.totals):
+        # scan.cpp:43-44, decided from the plan identically on every rank
+        raise plz.ValidationError("block too large: offsets exceed 4-byte table range")
     local, my_segs = backend.assemble(plan.bases[comm.rank], stream)
     img = None
     if comm.rank == 0:
@@ -241,13 +276,25 @@ def decompress_sharded(backend, comm, img, gather: bool = True, stream: int = 0)
     slice's (offset, length); with `gather`, rank 0 receives every slice at its
     offset (P2P) into the whole output.  Returns (output on rank 0 else None,
     this rank's slice, its offset in the output)."""
-    total = backend.total_chunks(img, stream)
-    rng = chunk_ranges(total, comm.world)[comm.rank]
-    local, begin = backend.decode_range(img, rng, stream)
+    own, local, begin = None, None, 0
+    try:
+        total = backend.total_chunks(img, stream)
+        rng = chunk_ranges(total, comm.world)[comm.rank]
+        local, begin = backend.decode_range(img, rng, stream)
+    except plz.Error as e:
+        own = e
+    n_local = local.numel() if local is not None else 0
+    status = [tuple(v) for v in comm.allgather([_status_of(own) if own else 0, begin, n_local])]
+    if any(st for st, _, _ in status):
+        # the single-call decode raises exactly the reference's error (a
+        # later container's header error only after earlier containers'
+        # token errors, decoder.cpp:129-141) — every rank holds the image
+        backend.decode_all(img)
+        r = next(i for i, (st, _, _) in enumerate(status) if st)
+        _raise_remote(r, status[r][0], own if r == comm.rank else None)
     if not gather:
         return None, local, begin
-    n_local = local.numel()
-    sizes = [tuple(v) for v in comm.allgather([begin, n_local])]
+    sizes = [(b, n) for _, b, n in status]
     n_out = max((b + n for b, n in sizes), default=0)
     out, segs_by_rank = None, None
     if comm.rank == 0:

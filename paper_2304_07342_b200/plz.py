@@ -340,6 +340,7 @@ def compress(data, params: Params, threads: int = 0, stats: Optional[PipelineSta
         t = data.contiguous().view(torch.uint8).reshape(-1)
         n = t.numel()
         if t.is_cuda:
+            ctx = context(t.device.index)  # the tensor's GPU, whatever the current device
             cap = compress_bound(n, params)
             out = torch.empty(max(cap, 1), dtype=torch.uint8, device=t.device)
             ln, st = ctx.compress_ptr(params, t.data_ptr(), n, out.data_ptr(), cap,
@@ -367,6 +368,7 @@ def decompress_bytes(img, threads: int = 0):
 
         t = img.contiguous().view(torch.uint8).reshape(-1)
         if t.is_cuda:
+            ctx = context(t.device.index)
             stream = torch.cuda.current_stream(t.device).cuda_stream
             cap = ctx.decompressed_size(t.data_ptr(), t.numel(), stream)  # device parse
             out = torch.empty(max(cap, 16), dtype=torch.uint8, device=t.device)
@@ -394,6 +396,10 @@ def compress_multi(data, params: Params, devices: Sequence[int],
         t = data.contiguous().view(torch.uint8).reshape(-1)
         cap = compress_bound(t.numel(), params)
         out = torch.empty(max(cap, 16), dtype=torch.uint8, device=torch.device("cuda", devices[0]))
+        # the ranks run on the library's own streams: the input (and the
+        # output allocation) must be complete before the call
+        torch.cuda.current_stream(t.device).synchronize()
+        torch.cuda.current_stream(out.device).synchronize()
         _check(L.lib().plzgpu_compress_multi(devs, len(devices), C.byref(params.to_c()),
                                              C.c_void_p(t.data_ptr()), t.numel(),
                                              C.c_void_p(out.data_ptr()), out.numel(), C.byref(ln),
@@ -423,9 +429,11 @@ def decompress_multi(img, devices: Sequence[int]):
         import torch
 
         t = img.contiguous().view(torch.uint8).reshape(-1)
-        cap = context().decompressed_size(t.data_ptr(), t.numel(),
-                                          torch.cuda.current_stream(t.device).cuda_stream)
+        cap = context(t.device.index).decompressed_size(
+            t.data_ptr(), t.numel(), torch.cuda.current_stream(t.device).cuda_stream)
         out = torch.empty(max(cap, 16), dtype=torch.uint8, device=torch.device("cuda", devices[0]))
+        torch.cuda.current_stream(t.device).synchronize()
+        torch.cuda.current_stream(out.device).synchronize()
         _check(L.lib().plzgpu_decompress_multi(devs, len(devices), C.c_void_p(t.data_ptr()),
                                                t.numel(), C.c_void_p(out.data_ptr()), out.numel(),
                                                C.byref(ln), C.byref(e)), e)
@@ -445,8 +453,8 @@ def decompress_range(img, chunk_begin: int, chunk_end: int):
     dist.decompress_sharded."""
     import torch
 
-    ctx = context()
     t = img.contiguous().view(torch.uint8).reshape(-1)
+    ctx = context(t.device.index)
     stream = torch.cuda.current_stream(t.device).cuda_stream
     _, ln, _ = ctx.decompress_range(t.data_ptr(), t.numel(), chunk_begin, chunk_end, 0, 0, stream)
     out = torch.empty(max(ln, 16), dtype=torch.uint8, device=t.device)

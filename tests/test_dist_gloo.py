@@ -17,6 +17,13 @@ from paper_2304_07342_b200 import dist as D
 from paper_2304_07342_b200 import plz
 
 
+def _as_plz(e: "O.OracleError") -> plz.Error:
+    """The oracle's error as the plz exception of the same code."""
+    cls = {1: plz.ValidationError, 2: plz.UnsupportedFormatError, 3: plz.CorruptionError,
+           4: plz.ContractError}.get(e.info.code, plz.Error)
+    return cls(e.info.message)
+
+
 class OracleBackend:
     """Per-rank pieces taken from a reference image (test stand-in for the
     GPU kernels; the protocol code under test is dist.py + the C-ABI's
@@ -34,6 +41,7 @@ class OracleBackend:
             self.conts.append((n, pt, ft, fs, fs + ft[n]))
             at = fs + ft[n] + pt[n] + image[at + 25]
         self.cpb = params.block_bytes // (params.chunk_size * params.symbol_width)
+        self.rank, self.fail_rank = 0, -1
 
     # ---- sharded decompress: the range semantics restated over the image's
     # headers and the oracle's whole-image decode
@@ -53,11 +61,19 @@ class OracleBackend:
     def total_chunks(self, img, stream=0):
         return len(self._starts()[0])
 
+    def decode_all(self, img):
+        try:
+            return O.decompress(self.img)
+        except O.OracleError as e:
+            raise _as_plz(e) from None
+
     def decode_range(self, img, rng, stream=0):
         starts, total_out = self._starts()
         start = lambda g: 0 if g == 0 else (total_out if g >= len(starts) else starts[g])  # noqa: E731
         lo, hi = start(rng[0]), start(rng[1])
-        full = O.decompress(self.img)
+        if self.fail_rank == self.rank:  # a token error inside this rank's range only
+            raise plz.CorruptionError("corrupt chunk (stand-in for a range decode error)", 0, 0, 0)
+        full = self.decode_all(img)
         return torch.frombuffer(bytearray(full[lo:hi]) or bytearray(1), dtype=torch.uint8)[:hi - lo], lo
 
     def _touched(self, rng):
@@ -192,3 +208,48 @@ def test_shard_protocol_over_gloo(world):
         pr.join(120)
     assert all(pr.exitcode == 0 for pr in procs)
     assert q.get(timeout=5) == [True] * len(CASES)
+
+
+def _worker_err(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        S, W, Cs, I, bb, size = CASES[0]
+        p = plz.validate(plz.Params(S, W, Cs, I, bb))
+        data = inputs.make("quant", size, 13, S)
+        image = bytearray(O.compress(data, O.make_params(S, W, Cs, I, bb)))
+        image = image[:-1]  # truncated streams in the last container
+        try:
+            O.decompress(bytes(image))
+            want = None
+        except O.OracleError as e:
+            want = (e.info.code, e.info.message)
+        be = OracleBackend(p, bytes(image))
+        be.rank, be.fail_rank = rank, world - 1  # only the last rank's range fails
+        try:
+            D.decompress_sharded(be, D.TorchComm("cpu"), None)
+            got = None
+        except plz.Error as e:
+            got = (type(e).__name__, str(e))
+        q.put((rank, want, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_decompress_error_reaches_every_rank(world):
+    # one rank's range fails: every rank raises the single-call error (no
+    # rank waits in a collective), matching the reference decoder's message
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + world + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker_err, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    res = [q.get(timeout=5) for _ in range(world)]
+    for rank, want, got in res:
+        assert want is not None and got is not None
+        assert got == ("CorruptionError", want[1])

@@ -42,3 +42,18 @@ def test_reference_acceptance_suite_on_the_b200_dropin():
             assert "identical across {1,2,4,8} threads: yes" in ln, ln
         else:
             assert ln.startswith("[PASS]"), ln
+
+
+CB = os.path.join(os.path.dirname(BIN), "compress_block_on_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(CB), reason="compress_block_on_b200 not built")
+def test_compress_block_matches_reference_compress_block():
+    # plz::compress_block (pipeline.hpp:22-24) of the drop-in against the
+    # reference's plzref::compress_block (pipeline.cpp:26-86) for every block
+    # of plz::plan over a parameter grid: non-final and final blocks, partial
+    # last chunks, raw tails and tail-only blocks, plus the contract_error
+    # of a span that does not match its plan (tests/cpp/compress_block_parity.cpp)
+    r = subprocess.run([CB], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert ", 0 failures" in r.stdout
