@@ -206,9 +206,17 @@ def rlib():
     return _rlib
 
 
-def _take(ptr: C.c_void_p, n: int) -> bytes:
+def _take(ptr: C.c_void_p, n: int):
+    """The malloc'd result as bytes (a numpy uint8 array past 1 GiB, where
+    ctypes.string_at's int size overflows)."""
     try:
-        return C.string_at(ptr, n) if n else b""
+        if n < (1 << 30):
+            return C.string_at(ptr, n) if n else b""
+        import numpy as np
+
+        out = np.empty(n, dtype=np.uint8)
+        C.memmove(out.ctypes.data, ptr, n)
+        return out
     finally:
         rlib().plzref_free(ptr)
 
