@@ -34,6 +34,15 @@ constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 K
 // memory)
 constexpr uint32_t kDecodePad = 128;
 constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSmem / 8;
+// The decode kernel's per-warp region (decode_chunk_fast): output stage
+// (kDecodeSmem bytes), token table (one byte per token: a pointer's offset,
+// 0 for a literal; a chunk has at most C = kDecodeSmem / S tokens), wave
+// table (per 32 output positions: token-start bitmap + address of the token
+// before the wave, bit 31 = in-wave sources), chase bits (one per wave).
+constexpr uint32_t kFastPtab = kDecodeSmem;
+constexpr uint32_t kFastMeta = 2 * kDecodeSmem;
+constexpr uint32_t kFastChase = kFastMeta + kDecodeSmem / 4;
+constexpr uint32_t kFastWarpSmem = kFastChase + kDecodeSmem / 256;
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -394,6 +403,161 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
     return TE_OK;
 }
 
+// ------------------------------------------------------- fast chunk decode
+// decode_chunk_fast: the decode kernel's chunk routine for chunks whose
+// output fits the warp's stage.  Same token semantics as decode_chunk_smem
+// (decoder.cpp:22-90), but it only answers "does the reference walk accept
+// this chunk" — on any failure the chunk is reported and plz_chunk_detail_kernel
+// re-walks it with decode_chunk_smem for the exact error and token — which
+// lets it run in two lean phases instead of interleaving them per batch:
+//
+//  A. tokens, 32 per step (lane = token): flag bit, payload field through a
+//     128-byte window of aligned words (one per lane, shuffles), an inclusive
+//     scan of token lengths for output positions; literals go straight to
+//     the stage, every token start is set in its wave's start bitmap and its
+//     offset (0 for a literal) lands in the token table; a pointer whose
+//     source may lie in its own 32-position wave (off < 32) marks that wave.
+//  B. waves of 32 output positions in order: one shared load of the wave's
+//     bitmap + token base, a popcount gives each lane its covering token, one
+//     byte load its offset, and the lane copies out[q - off] (a literal
+//     position copies onto itself).  Only marked waves resolve in-wave
+//     sources, by pointer jumping over the lanes' sources.
+// Lookups for four waves are issued ahead of their copies (they read only
+// phase A's tables), so the copies chain through shared memory back to back.
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+template <int S>
+__device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf,
+                                  const uint8_t* __restrict__ pay, uint32_t np, uint32_t L,
+                                  uint8_t* wsm, uint32_t lane) {
+    constexpr uint32_t FULL = 0xffffffffu;
+    uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);    // pairs {starts, base}
+    uint32_t* chase = reinterpret_cast<uint32_t*>(wsm + kFastChase);
+    const uint32_t s_stage = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
+    const uint32_t s_ptab = s_stage + kFastPtab;
+    const uint32_t s_meta = s_stage + kFastMeta;
+    const uint32_t nwv = (L + 31u) >> 5;
+    for (uint32_t w = lane; w < nwv; w += 32) meta[2 * w] = 0u;
+    if (lane < kDecodeSmem / 1024) chase[lane] = 0u;
+    __syncwarp();
+    // ---- phase A
+    const uint32_t below = (1u << lane) - 1u;
+    uint32_t written = 0, in = 0, t = 0;
+    uint32_t fbyte = (lane >> 3) < nf ? flags[lane >> 3] : 0u;
+    uint32_t win = load_window(pay, np, 0, lane);
+    while (written < L) {
+        const uint32_t tt = t + lane;
+        const bool hf = (tt >> 3) < nf;
+        const uint32_t bit = hf ? (fbyte >> (7u - (tt & 7u))) & 1u : 0u;
+        const uint32_t pmask = __ballot_sync(FULL, bit);
+        const uint32_t nptr = __popc(pmask & below);
+        const uint32_t pin = in + 2u * nptr + uint32_t(S) * (lane - nptr);
+        const uint32_t sz = bit ? 2u : uint32_t(S);
+        const bool has = pin + sz <= np;
+        const uint32_t o = pin - in + uint32_t(reinterpret_cast<uintptr_t>(pay + in) & 3u);
+        const uint32_t wa = __shfl_sync(FULL, win, (o >> 2) & 31u);
+        const uint32_t wb = __shfl_sync(FULL, win, ((o >> 2) + 1u) & 31u);
+        uint32_t v = __funnelshift_r(wa, wb, 8u * (o & 3u));
+        if (S == 4 && o + sz > 128u && has) {  // past the window (32 misaligned literals)
+            v = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (uint32_t(b) < sz) v |= uint32_t(pay[pin + b]) << (8 * b);
+        }
+        const uint32_t len = bit ? (v & 0xffu) : 1u;
+        const uint32_t off = bit ? ((v >> 8) & 0xffu) : 0u;
+        const uint32_t incl = warp_incl_scan_u32(len, lane);
+        const uint32_t pos = written + incl - len;
+        const bool reached = pos < L;
+        const bool bad = !hf || !has || (bit && (len == 0u || off == 0u || off > pos || pos + len > L));
+        // reached lanes form a prefix (positions never decrease)
+        if (__ballot_sync(FULL, bad && reached)) return false;
+        const uint32_t m_end = __ballot_sync(FULL, !reached);
+        const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
+        if (reached) {
+            if (!bit) sts_sym<S>(s_stage + pos * S, S == 4 ? v : v & ((1u << (8 * S)) - 1u));
+            atomicOr(&meta[2 * (pos >> 5)], 1u << (pos & 31u));
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(s_ptab + tt), "r"(off));
+            if (bit && off < 32u) {
+                const uint32_t w0 = pos >> 5, w1 = (pos + len - 1u) >> 5;
+                if (len <= off) {
+                    atomicOr(&chase[w0 >> 5], 1u << (w0 & 31u));
+                    if (w1 != w0) atomicOr(&chase[w1 >> 5], 1u << (w1 & 31u));
+                } else {  // replicating pointer (len > off): every wave it covers
+                    for (uint32_t w = w0; w <= w1; ++w) atomicOr(&chase[w >> 5], 1u << (w & 31u));
+                }
+            }
+        }
+        const uint32_t la = first_end - 1u;
+        const uint32_t span = __shfl_sync(FULL, incl, la);
+        in = __shfl_sync(FULL, pin + sz, la);
+        t += first_end;
+        if (written + span < L) {  // the next step's loads, ahead of the bookkeeping
+            const uint32_t fi = (t + lane) >> 3;
+            fbyte = fi < nf ? flags[fi] : 0u;
+            win = load_window(pay, np, in, lane);
+        }
+        written += span;
+    }
+    // the walk's end checks (decoder.cpp:58-65)
+    if (in != np || nf != ((t + 7u) >> 3)) return false;
+    if ((t & 7u) && (flags[t >> 3] & (0xffu >> (t & 7u)))) return false;
+    __syncwarp();
+    // ---- wave table: tokens before each wave (scan of the bitmaps' popcounts)
+    uint32_t carry = 0;
+    for (uint32_t w0 = 0; w0 < nwv; w0 += 32) {
+        const uint32_t w = w0 + lane;
+        const uint32_t c = w < nwv ? __popc(meta[2 * w]) : 0u;
+        const uint32_t inc = warp_incl_scan_u32(c, lane);
+        if (w < nwv)
+            meta[2 * w + 1] = (s_ptab + carry + inc - c - 1u) | (((chase[w >> 5] >> (w & 31u)) & 1u) << 31);
+        carry += __shfl_sync(FULL, inc, 31);
+    }
+    __syncwarp();
+    // ---- phase B
+    const uint32_t upto = (2u << lane) - 1u;
+    uint32_t a_q = s_stage + lane * uint32_t(S);
+    for (uint32_t w4 = 0; w4 < nwv; w4 += 4) {
+        uint32_t offs[4], flagsw[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t st = 0, tb = 0;
+            if (w4 + k < nwv)
+                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
+                             : "=r"(st), "=r"(tb) : "r"(s_meta + 8u * (w4 + k)));
+            flagsw[k] = tb;
+            offs[k] = w4 + k < nwv ? lds_u8((tb & 0x7fffffffu) + __popc(st & upto)) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (w4 + k >= nwv) continue;
+            uint32_t val;
+            if (flagsw[k] & 0x80000000u) {  // sources inside the wave: pointer jumping
+                const int wb = int((w4 + k) << 5);
+                int src = wb + int(lane) - int(offs[k]);
+                bool more;
+                do {
+                    const bool inw = src >= wb;
+                    const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
+                    more = inw && s2 != src;
+                    src = inw ? s2 : src;
+                } while (__any_sync(FULL, more));
+                val = lds_sym<S>(s_stage + uint32_t(src) * S);
+            } else {
+                val = lds_sym<S>(a_q - offs[k] * S);
+            }
+            sts_sym<S>(a_q, val);
+            a_q += 32u * S;
+            __syncwarp();
+        }
+    }
+    return true;
+}
+
 // ------------------------------------------------------------------ parse
 enum ParseErr : uint32_t {
     PE_OK = 0,
@@ -633,7 +797,10 @@ __device__ __forceinline__ bool wait_image(const DecodePipe& a, uint64_t b, uint
     return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 
-template <int S, bool kPipe>
+// kExact: the error detail path (exact TokenErr and token index); otherwise
+// chunks that fit the stage take decode_chunk_fast and a failure is reported
+// as TE_FLAGS_EXHAUSTED, a placeholder the detail kernel replaces.
+template <int S, bool kPipe, bool kExact>
 __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const ContainerDesc& d,
                                                      uint64_t k, uint8_t* stage, uint32_t lane,
                                                      uint64_t* err_tok, const DecodePipe& pp) {
@@ -680,7 +847,10 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint64_t tok = 0;
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
-    if (in_smem)
+    if (!kExact && in_smem)
+        e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
+                ? TE_OK : TE_FLAGS_EXHAUSTED;
+    else if (in_smem)
         e = decode_chunk_smem<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L),
                                  static_cast<uint32_t>(__cvta_generic_to_shared(stage)),
                                  static_cast<uint32_t>(__cvta_generic_to_shared(tab)),
@@ -721,7 +891,7 @@ __device__ __forceinline__ uint64_t find_container(const ContainerDesc* desc, ui
     return lo;
 }
 
-template <bool kPipe = false>
+template <bool kPipe = false, bool kExact = false>
 __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uint64_t g,
                                                         uint8_t* stage, uint32_t lane,
                                                         uint64_t* k, uint64_t* tok,
@@ -729,9 +899,9 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
     const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
     *k = g - d.chunk_base;
     switch (d.S) {
-        case 1: return decode_one_chunk<1, kPipe>(a, d, *k, stage, lane, tok, pp);
-        case 2: return decode_one_chunk<2, kPipe>(a, d, *k, stage, lane, tok, pp);
-        default: return decode_one_chunk<4, kPipe>(a, d, *k, stage, lane, tok, pp);
+        case 1: return decode_one_chunk<1, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
+        case 2: return decode_one_chunk<2, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
+        default: return decode_one_chunk<4, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
     }
 }
 
@@ -740,7 +910,7 @@ template <bool kPipe>
 __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = lane_id();
-    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kDecodeWarpSmem;
+    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kFastWarpSmem;
     const uint64_t total = a.result->total_chunks;
     for (;;) {
         uint64_t g = 0;
@@ -808,7 +978,7 @@ __global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* 
     extern __shared__ __align__(16) uint8_t smem[];
     const uint64_t g = *a.err_chunk;
     uint64_t k = 0, tok = 0;
-    const uint32_t e = decode_global_chunk(a, g, smem, lane_id(), &k, &tok);
+    const uint32_t e = decode_global_chunk<false, true>(a, g, smem, lane_id(), &k, &tok);
     if (lane_id() == 0) {
         *code = e;
         *chunk = k;
@@ -860,7 +1030,7 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 
 int decode_ctas_per_sm() {
     int blocks = 0;
-    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
+    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel<false>, kDecodeWarps * 32,
                                                   smem);
     return blocks;
@@ -871,7 +1041,7 @@ void launch_parse(const DecodeArgs& a, cudaStream_t st) {
 }
 
 void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
+    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
     plz_decode_kernel<false><<<grid, kDecodeWarps * 32, smem, st>>>(a, DecodePipe{});
 }
 
@@ -881,7 +1051,7 @@ void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, u
 }
 
 void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st) {
-    const size_t smem = size_t(kDecodeWarps) * kDecodeWarpSmem;
+    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
     plz_decode_kernel<true><<<grid, kDecodeWarps * 32, smem, st>>>(a, pp);
 }
 
