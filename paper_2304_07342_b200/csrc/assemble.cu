@@ -64,36 +64,31 @@ __device__ __forceinline__ uint4 funnel128(const uint4& lo, const uint4& hi, uin
 // Word w of a job: the aligned 16-byte destination word W0 + 16w (W0 = dst
 // rounded down); its bytes come from source bytes [16w - m, 16w - m + 16),
 // m = dst & 15, i.e. source words w - 1 and w (word -1 reads as zeros: its
-// bytes lie before dst and are never stored).
-struct Word {
-    uint4 lo, hi;
-    uint8_t* at;   // aligned destination
-    int32_t b0, b1;  // valid destination bytes [b0, b1) of the word
-    uint32_t m;
-};
-
-__device__ __forceinline__ void load_word(const Job& j, uint32_t w, Word& o) {
+// bytes lie before dst and are never stored).  Only the source words are
+// kept between the load and the store (registers: 4 words per lane).
+__device__ __forceinline__ void load_word(const Job& j, uint32_t w, uint4& lo, uint4& hi) {
     const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(j.dst) & 15u);
     const uint4* s16 = reinterpret_cast<const uint4*>(j.src);
-    o.m = m;
-    o.at = j.dst - m + 16u * w;
-    o.b0 = w == 0 ? int32_t(m) : 0;
-    const int32_t end = int32_t(m + j.len) - int32_t(16u * w);
-    o.b1 = end < 16 ? end : 16;
-    o.hi = __ldg(s16 + w);
-    o.lo = (m && w) ? __ldg(s16 + w - 1) : make_uint4(0, 0, 0, 0);
+    hi = __ldg(s16 + w);
+    lo = (m && w) ? __ldg(s16 + w - 1) : make_uint4(0, 0, 0, 0);
 }
 
-__device__ __forceinline__ void store_word(const Word& o) {
-    const uint4 v = o.m ? funnel128(o.lo, o.hi, 16u - o.m) : o.hi;
-    if (o.b0 == 0 && o.b1 == 16) {
-        *reinterpret_cast<uint4*>(o.at) = v;
+__device__ __forceinline__ void store_word(const Job& j, uint32_t w, const uint4& lo,
+                                           const uint4& hi) {
+    const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(j.dst) & 15u);
+    uint8_t* at = j.dst - m + 16u * w;
+    const int32_t b0 = w == 0 ? int32_t(m) : 0;
+    const int32_t end = int32_t(m + j.len) - int32_t(16u * w);
+    const int32_t b1 = end < 16 ? end : 16;
+    const uint4 v = m ? funnel128(lo, hi, 16u - m) : hi;
+    if (b0 == 0 && b1 == 16) {
+        *reinterpret_cast<uint4*>(at) = v;
         return;
     }
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
     for (int b = 0; b < 16; ++b)
-        if (b >= o.b0 && b < o.b1) o.at[b] = uint8_t(wv[b >> 2] >> (8 * (b & 3)));
+        if (b >= b0 && b < b1) at[b] = uint8_t(wv[b >> 2] >> (8 * (b & 3)));
 }
 
 // One warp copies two jobs (a chunk's flag and payload slices): up to 4
@@ -101,15 +96,17 @@ __device__ __forceinline__ void store_word(const Word& o) {
 __device__ __forceinline__ void warp_copy2(const Job& j0, const Job& j1, uint32_t lane) {
     const uint32_t n0 = job_words(j0), n = n0 + job_words(j1);
     for (uint32_t base = 0; base < n; base += 128) {
-        Word w[4];
+        uint4 lo[4], hi[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint32_t i = base + lane + 32u * u;
-            if (i < n) load_word(i < n0 ? j0 : j1, i < n0 ? i : i - n0, w[u]);
+            if (i < n) load_word(i < n0 ? j0 : j1, i < n0 ? i : i - n0, lo[u], hi[u]);
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (base + lane + 32u * u < n) store_word(w[u]);
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t i = base + lane + 32u * u;
+            if (i < n) store_word(i < n0 ? j0 : j1, i < n0 ? i : i - n0, lo[u], hi[u]);
+        }
     }
 }
 
@@ -163,7 +160,7 @@ __device__ __forceinline__ uint64_t container_start(const AssembleArgs& a, uint6
     return 26u * j + 8u * (g0 + j) + a.P64[g0] + a.F64[g0];
 }
 
-__global__ void __launch_bounds__(256) plz_assemble_kernel(AssembleArgs a) {
+__global__ void __launch_bounds__(256, 3) plz_assemble_kernel(AssembleArgs a) {
     const uint32_t lane = lane_id();
     const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
     // ---- offset tables: both tables of container j are one region of
@@ -246,6 +243,10 @@ __global__ void plz_headers_kernel(AssembleArgs a) {
     st_le32(h + 17, uint32_t(byte_len >> 32));
     st_le32(h + 21, uint32_t(n));
     h[25] = uint8_t(tail);
+    // the final table entries (also written by Kernel III's table pass, which
+    // does not run for an input without chunks)
+    st_le32(h + 26 + 4 * n, uint32_t(ptot));
+    st_le32(h + 26 + 4 * (n + 1) + 4 * n, uint32_t(ftot));
     uint8_t* t = h + 26 + 8 * (n + 1) + ftot + ptot;
     const uint8_t* src = a.in + j * a.block_bytes + byte_len - tail;
     for (uint32_t i = 0; i < tail; ++i) t[i] = src[i];
@@ -262,7 +263,7 @@ __device__ __forceinline__ uint64_t find_cont(const ShardAssembleArgs& a, uint64
     return c;
 }
 
-__global__ void __launch_bounds__(256) plz_shard_assemble_kernel(ShardAssembleArgs a) {
+__global__ void __launch_bounds__(256, 4) plz_shard_assemble_kernel(ShardAssembleArgs a) {
     const uint32_t lane = lane_id();
     // ---- table slices: per touched container, its payload-table slice then
     // its flag-table slice, g_hi - g_lo entries each

@@ -25,7 +25,7 @@
 namespace plzgpu {
 namespace {
 
-constexpr int kDecodeWarps = 8;
+constexpr int kDecodeWarps = 4;
 constexpr uint32_t kDecodeSmem = 4096;  // bytes of output staging per warp (4 KiB chunks;
                                         // larger chunks decode in global memory)
 // + pad (a wave writes up to 31 positions past its batch's span) + token
@@ -36,13 +36,18 @@ constexpr uint32_t kDecodePad = 128;
 constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSmem / 8;
 // The decode kernel's per-warp region (decode_chunk_fast): output stage
 // (kDecodeSmem bytes), token table (one byte per token: a pointer's offset,
-// 0 for a literal; a chunk has at most C = kDecodeSmem / S tokens), wave
-// table (per 32 output positions: token-start bitmap + address of the token
-// before the wave, bit 31 = in-wave sources), chase bits (one per wave).
+// 0 for a literal; kFastTokens entries — a chunk with more flag bits than
+// that takes decode_chunk_smem), wave table (per 32 output positions:
+// token-start bitmap + address of the token before the wave, bit 31 =
+// in-wave sources possible), chase bits (one per wave).
+constexpr uint32_t kFastTokens = 2048;
 constexpr uint32_t kFastPtab = kDecodeSmem;
-constexpr uint32_t kFastMeta = 2 * kDecodeSmem;
+constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
 constexpr uint32_t kFastChase = kFastMeta + kDecodeSmem / 4;
 constexpr uint32_t kFastWarpSmem = kFastChase + kDecodeSmem / 256;
+static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
+constexpr bool kUseFast = true;
+constexpr uint32_t kMainWarpSmem = kUseFast ? kFastWarpSmem : kDecodeWarpSmem;
 
 __device__ __forceinline__ uint32_t warp_incl_scan_u32(uint32_t v, uint32_t lane) {
 #pragma unroll
@@ -408,26 +413,30 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
 // output fits the warp's stage.  Same token semantics as decode_chunk_smem
 // (decoder.cpp:22-90), but it only answers "does the reference walk accept
 // this chunk" — on any failure the chunk is reported and plz_chunk_detail_kernel
-// re-walks it with decode_chunk_smem for the exact error and token — which
-// lets it run in two lean phases instead of interleaving them per batch:
+// re-walks it with decode_chunk_smem for the exact error and token — so it
+// runs in two lean phases:
 //
-//  A. tokens, 32 per step (lane = token): flag bit, payload field through a
-//     128-byte window of aligned words (one per lane, shuffles), an inclusive
-//     scan of token lengths for output positions; literals go straight to
-//     the stage, every token start is set in its wave's start bitmap and its
-//     offset (0 for a literal) lands in the token table; a pointer whose
-//     source may lie in its own 32-position wave (off < 32) marks that wave.
+//  A. tokens, 256 per step: lane l owns flag byte l of the step and walks its
+//     8 tokens itself (their payload fields are contiguous: S = 2 reads its 16
+//     bytes as 5 aligned words, other widths byte by byte), so one warp scan
+//     per 256 tokens places them.  Literals go straight to the stage, every
+//     token start is set in its wave's start bitmap and its offset (0 for a
+//     literal) lands in the token table; a pointer whose source may lie in its
+//     own 32-position wave (off < 32) marks that wave.
 //  B. waves of 32 output positions in order: one shared load of the wave's
 //     bitmap + token base, a popcount gives each lane its covering token, one
 //     byte load its offset, and the lane copies out[q - off] (a literal
-//     position copies onto itself).  Only marked waves resolve in-wave
-//     sources, by pointer jumping over the lanes' sources.
-// Lookups for four waves are issued ahead of their copies (they read only
-// phase A's tables), so the copies chain through shared memory back to back.
+//     position copies onto itself).  In a marked wave the lanes first check
+//     whether any source is an in-wave pointer position and only then resolve
+//     by pointer jumping over the lanes' sources.
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
     return v;
+}
+
+__device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t v, uint32_t lane) {
+    return warp_incl_scan_u32(v, lane) - v;
 }
 
 template <int S>
@@ -435,7 +444,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                                   const uint8_t* __restrict__ pay, uint32_t np, uint32_t L,
                                   uint8_t* wsm, uint32_t lane) {
     constexpr uint32_t FULL = 0xffffffffu;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);    // pairs {starts, base}
+    uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);  // pairs {starts, base}
     uint32_t* chase = reinterpret_cast<uint32_t*>(wsm + kFastChase);
     const uint32_t s_stage = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
     const uint32_t s_ptab = s_stage + kFastPtab;
@@ -445,67 +454,116 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     if (lane < kDecodeSmem / 1024) chase[lane] = 0u;
     __syncwarp();
     // ---- phase A
-    const uint32_t below = (1u << lane) - 1u;
-    uint32_t written = 0, in = 0, t = 0;
-    uint32_t fbyte = (lane >> 3) < nf ? flags[lane >> 3] : 0u;
-    uint32_t win = load_window(pay, np, 0, lane);
-    while (written < L) {
-        const uint32_t tt = t + lane;
-        const bool hf = (tt >> 3) < nf;
-        const uint32_t bit = hf ? (fbyte >> (7u - (tt & 7u))) & 1u : 0u;
-        const uint32_t pmask = __ballot_sync(FULL, bit);
-        const uint32_t nptr = __popc(pmask & below);
-        const uint32_t pin = in + 2u * nptr + uint32_t(S) * (lane - nptr);
-        const uint32_t sz = bit ? 2u : uint32_t(S);
-        const bool has = pin + sz <= np;
-        const uint32_t o = pin - in + uint32_t(reinterpret_cast<uintptr_t>(pay + in) & 3u);
-        const uint32_t wa = __shfl_sync(FULL, win, (o >> 2) & 31u);
-        const uint32_t wb = __shfl_sync(FULL, win, ((o >> 2) + 1u) & 31u);
-        uint32_t v = __funnelshift_r(wa, wb, 8u * (o & 3u));
-        if (S == 4 && o + sz > 128u && has) {  // past the window (32 misaligned literals)
-            v = 0;
+    uint32_t written = 0, in = 0, tbase = 0, T = 0, in_end = 0;
+    for (uint32_t fb0 = 0;; fb0 += 32) {
+        const uint32_t fidx = fb0 + lane;
+        const bool hf = fidx < nf;
+        const uint32_t fb = hf ? uint32_t(flags[fidx]) : 0u;
+        uint32_t pin, wv[4] = {0u, 0u, 0u, 0u};
+        if constexpr (S == 2) {
+            pin = in + 16u * lane;  // every token is 2 payload bytes
+            const uintptr_t a = reinterpret_cast<uintptr_t>(pay) + pin;
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+            const uintptr_t lim = reinterpret_cast<uintptr_t>(pay) + np;
+            uint32_t x[5];
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (uint32_t(b) < sz) v |= uint32_t(pay[pin + b]) << (8 * b);
+            for (int k = 0; k < 5; ++k)
+                x[k] = reinterpret_cast<uintptr_t>(wp + k) < lim ? wp[k] : 0u;
+            const uint32_t sh = 8u * uint32_t(a & 3u);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) wv[k] = __funnelshift_r(x[k], x[k + 1], sh);
+        } else {
+            const uint32_t p = __popc(fb);
+            pin = in + warp_excl_scan_u32(2u * p + uint32_t(S) * (8u - p), lane);
         }
-        const uint32_t len = bit ? (v & 0xffu) : 1u;
-        const uint32_t off = bit ? ((v >> 8) & 0xffu) : 0u;
-        const uint32_t incl = warp_incl_scan_u32(len, lane);
-        const uint32_t pos = written + incl - len;
-        const bool reached = pos < L;
-        const bool bad = !hf || !has || (bit && (len == 0u || off == 0u || off > pos || pos + len > L));
-        // reached lanes form a prefix (positions never decrease)
-        if (__ballot_sync(FULL, bad && reached)) return false;
-        const uint32_t m_end = __ballot_sync(FULL, !reached);
-        const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
-        if (reached) {
-            if (!bit) sts_sym<S>(s_stage + pos * S, S == 4 ? v : v & ((1u << (8 * S)) - 1u));
-            atomicOr(&meta[2 * (pos >> 5)], 1u << (pos & 31u));
-            asm volatile("st.shared.u8 [%0], %1;" ::"r"(s_ptab + tt), "r"(off));
-            if (bit && off < 32u) {
-                const uint32_t w0 = pos >> 5, w1 = (pos + len - 1u) >> 5;
-                if (len <= off) {
-                    atomicOr(&chase[w0 >> 5], 1u << (w0 & 31u));
-                    if (w1 != w0) atomicOr(&chase[w1 >> 5], 1u << (w1 & 31u));
-                } else {  // replicating pointer (len > off): every wave it covers
-                    for (uint32_t w = w0; w <= w1; ++w) atomicOr(&chase[w >> 5], 1u << (w & 31u));
-                }
+        // pass 1: token fields and lengths (S = 2 re-derives them from the
+        // four payload words in pass 2 instead of keeping 24 registers)
+        uint32_t lpk[2] = {0u, 0u}, opk[2] = {0u, 0u};  // other widths: lengths / offsets, 4 per word
+        uint32_t adv = 0, o = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t bit = (fb >> (7 - i)) & 1u;
+            uint32_t f;
+            if constexpr (S == 2) {
+                f = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
+                adv += bit ? (f & 0xffu) : 1u;
+                continue;
+            } else {
+                f = 0;
+                const uint32_t sz = bit ? 2u : uint32_t(S);
+#pragma unroll
+                for (int b = 0; b < (S > 2 ? S : 2); ++b)
+                    if (uint32_t(b) < sz && pin + o + uint32_t(b) < np)
+                        f |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
+                o += sz;
             }
+            const uint32_t len = bit ? (f & 0xffu) : 1u;
+            lpk[i >> 2] |= len << (8 * (i & 3));
+            opk[i >> 2] |= (bit ? ((f >> 8) & 0xffu) : 0u) << (8 * (i & 3));
+            adv += len;
         }
-        const uint32_t la = first_end - 1u;
-        const uint32_t span = __shfl_sync(FULL, incl, la);
-        in = __shfl_sync(FULL, pin + sz, la);
-        t += first_end;
-        if (written + span < L) {  // the next step's loads, ahead of the bookkeeping
-            const uint32_t fi = (t + lane) >> 3;
-            fbyte = fi < nf ? flags[fi] : 0u;
-            win = load_window(pay, np, in, lane);
+        uint32_t pos = written + warp_excl_scan_u32(adv, lane);
+        // pass 2: checks and writes (tokens from position L on are not read)
+        bool bad = false;
+        uint32_t nreach = 0, o_reach = 0;
+        o = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t bit = (fb >> (7 - i)) & 1u;
+            const uint32_t sz = bit ? 2u : uint32_t(S);
+            uint32_t len, off, fld;
+            if constexpr (S == 2) {
+                fld = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
+                len = bit ? (fld & 0xffu) : 1u;
+                off = bit ? (fld >> 8) : 0u;
+            } else {
+                len = (lpk[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                off = (opk[i >> 2] >> (8 * (i & 3))) & 0xffu;
+                fld = 0;
+                if (!bit)  // a literal's S bytes, read again
+#pragma unroll
+                    for (int b = 0; b < S; ++b)
+                        if (pin + o + uint32_t(b) < np) fld |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
+            }
+            const bool reached = pos < L;
+            const bool b = !hf || pin + o + sz > np ||
+                           (bit && (len == 0u || off == 0u || off > pos || pos + len > L));
+            bad |= reached && b;
+            if (reached && !b) {
+                const uint32_t t = tbase + 8u * lane + uint32_t(i);
+                if (!bit) sts_sym<S>(s_stage + pos * S, S == 4 ? fld : fld & ((1u << (8 * S)) - 1u));
+                atomicOr(&meta[2 * (pos >> 5)], 1u << (pos & 31u));
+                asm volatile("st.shared.u8 [%0], %1;" ::"r"(s_ptab + t), "r"(off));
+                if (bit && off < 32u) {
+                    const uint32_t w0 = pos >> 5, w1 = (pos + len - 1u) >> 5;
+                    if (len <= off) {
+                        atomicOr(&chase[w0 >> 5], 1u << (w0 & 31u));
+                        if (w1 != w0) atomicOr(&chase[w1 >> 5], 1u << (w1 & 31u));
+                    } else {  // replicating pointer (len > off): every wave it covers
+                        for (uint32_t w = w0; w <= w1; ++w) atomicOr(&chase[w >> 5], 1u << (w & 31u));
+                    }
+                }
+                ++nreach;
+                o_reach = o + sz;
+            }
+            pos += len;
+            o += sz;
         }
-        written += span;
+        if (__any_sync(FULL, bad)) return false;
+        const uint32_t end = __shfl_sync(FULL, pos, 31);
+        if (end >= L) {  // the walk ends in this step: tokens read, payload consumed
+            T = tbase + __reduce_add_sync(FULL, nreach);
+            const uint32_t m = __ballot_sync(FULL, nreach != 0u);
+            in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
+            break;
+        }
+        written = end;
+        in = __shfl_sync(FULL, pin + o, 31);
+        tbase += 256u;
     }
     // the walk's end checks (decoder.cpp:58-65)
-    if (in != np || nf != ((t + 7u) >> 3)) return false;
-    if ((t & 7u) && (flags[t >> 3] & (0xffu >> (t & 7u)))) return false;
+    if (in_end != np || nf != ((T + 7u) >> 3)) return false;
+    if ((T & 7u) && (flags[T >> 3] & (0xffu >> (T & 7u)))) return false;
     __syncwarp();
     // ---- wave table: tokens before each wave (scan of the bitmaps' popcounts)
     uint32_t carry = 0;
@@ -521,39 +579,32 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     // ---- phase B
     const uint32_t upto = (2u << lane) - 1u;
     uint32_t a_q = s_stage + lane * uint32_t(S);
-    for (uint32_t w4 = 0; w4 < nwv; w4 += 4) {
-        uint32_t offs[4], flagsw[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            uint32_t st = 0, tb = 0;
-            if (w4 + k < nwv)
-                asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];"
-                             : "=r"(st), "=r"(tb) : "r"(s_meta + 8u * (w4 + k)));
-            flagsw[k] = tb;
-            offs[k] = w4 + k < nwv ? lds_u8((tb & 0x7fffffffu) + __popc(st & upto)) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (w4 + k >= nwv) continue;
-            uint32_t val;
-            if (flagsw[k] & 0x80000000u) {  // sources inside the wave: pointer jumping
-                const int wb = int((w4 + k) << 5);
-                int src = wb + int(lane) - int(offs[k]);
+    for (uint32_t w = 0; w < nwv; ++w) {
+        uint32_t st, tb;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(st), "=r"(tb) : "r"(s_meta + 8u * w));
+        const uint32_t off = lds_u8((tb & 0x7fffffffu) + __popc(st & upto));
+        uint32_t val;
+        if (tb & 0x80000000u) {  // in-wave sources possible
+            const int wb = int(w << 5);
+            int src = wb + int(lane) - int(off);
+            // is any lane's source an in-wave POINTER position (not yet final)?
+            const uint32_t soff = __shfl_sync(FULL, off, uint32_t(src) & 31u);
+            if (__any_sync(FULL, src >= wb && soff != 0u)) {
                 bool more;
-                do {
+                do {  // pointer jumping over the lanes' sources
                     const bool inw = src >= wb;
                     const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
                     more = inw && s2 != src;
                     src = inw ? s2 : src;
                 } while (__any_sync(FULL, more));
-                val = lds_sym<S>(s_stage + uint32_t(src) * S);
-            } else {
-                val = lds_sym<S>(a_q - offs[k] * S);
             }
-            sts_sym<S>(a_q, val);
-            a_q += 32u * S;
-            __syncwarp();
+            val = lds_sym<S>(s_stage + uint32_t(src) * S);
+        } else {
+            val = lds_sym<S>(a_q - off * S);
         }
+        sts_sym<S>(a_q, val);
+        a_q += 32u * S;
+        __syncwarp();
     }
     return true;
 }
@@ -847,7 +898,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint64_t tok = 0;
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
-    if (!kExact && in_smem)
+    if (kUseFast && !kExact && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
     else if (in_smem)
@@ -891,6 +942,32 @@ __device__ __forceinline__ uint64_t find_container(const ContainerDesc* desc, ui
     return lo;
 }
 
+// kKind: which containers a decode kernel takes — kKindS2 the S = 2 ones
+// (decode_chunk_fast), kKindOther the rest (decode_chunk_smem), kKindAll
+// every one (the exact detail path).  Two specialised kernels keep the hot
+// S = 2 instance's registers at 56 instead of the 80 the union of all widths
+// needs (which would cost a fifth of the resident warps).
+constexpr int kKindOther = 0, kKindS2 = 1, kKindAll = 2;
+
+template <bool kPipe, bool kExact, int kKind>
+__device__ __forceinline__ uint32_t decode_desc_chunk(const DecodeArgs& a, const ContainerDesc& d,
+                                                      uint64_t k, uint8_t* stage, uint32_t lane,
+                                                      uint64_t* tok, const DecodePipe& pp) {
+    if constexpr (kKind == kKindS2) {
+        return decode_one_chunk<2, kPipe, kExact>(a, d, k, stage, lane, tok, pp);
+    } else {
+        switch (d.S) {
+            case 1: return decode_one_chunk<1, kPipe, true>(a, d, k, stage, lane, tok, pp);
+            case 2:
+                if constexpr (kKind == kKindAll)
+                    return decode_one_chunk<2, kPipe, true>(a, d, k, stage, lane, tok, pp);
+                else
+                    return TE_OK;  // not this kernel's container
+            default: return decode_one_chunk<4, kPipe, true>(a, d, k, stage, lane, tok, pp);
+        }
+    }
+}
+
 template <bool kPipe = false, bool kExact = false>
 __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uint64_t g,
                                                         uint8_t* stage, uint32_t lane,
@@ -898,27 +975,34 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
                                                         const DecodePipe& pp = DecodePipe{}) {
     const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
     *k = g - d.chunk_base;
-    switch (d.S) {
-        case 1: return decode_one_chunk<1, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
-        case 2: return decode_one_chunk<2, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
-        default: return decode_one_chunk<4, kPipe, kExact>(a, d, *k, stage, lane, tok, pp);
-    }
+    return decode_desc_chunk<kPipe, kExact, kKindAll>(a, d, *k, stage, lane, tok, pp);
 }
 
-// kPipe: the pipelined host path (per-chunk segment waits, output counts)
-template <bool kPipe>
+// kPipe: the pipelined host path (per-chunk segment waits, output counts).
+// Each kind has its own work counter (a.work[kind]); a warp that draws a
+// chunk of a container the kernel does not take moves the counter past that
+// container, so the other kernel's containers cost one draw each.
+template <bool kPipe, int kKind>
 __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
+    constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
     const uint32_t lane = lane_id();
-    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kFastWarpSmem;
+    uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kWarpSmem;
+    uint32_t* work = a.work + kKind;
     const uint64_t total = a.result->total_chunks;
     for (;;) {
         uint64_t g = 0;
-        if (lane == 0) g = atomicAdd(a.work, 1u);
+        if (lane == 0) g = atomicAdd(work, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= total) break;
-        uint64_t k, tok;
-        const uint32_t e = decode_global_chunk<kPipe>(a, g, stage, lane, &k, &tok, pp);
+        const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
+        if ((d.S == 2) != (kKind == kKindS2)) {
+            if (lane == 0) atomicMax(work, uint32_t(min(total, d.chunk_base + d.num_chunks)));
+            continue;
+        }
+        const uint64_t k = g - d.chunk_base;
+        uint64_t tok;
+        const uint32_t e = decode_desc_chunk<kPipe, false, kKind>(a, d, k, stage, lane, &tok, pp);
         if (e != TE_OK && lane == 0) atomicMin(a.err_chunk, (unsigned long long)g);
         if (kPipe) {
             // counted whatever the outcome (the D2H stream must never wait
@@ -926,7 +1010,6 @@ __global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArg
             __threadfence_system();
             __syncwarp();
             if (lane == 0) {
-                const ContainerDesc& d = a.desc[find_container(a.desc, a.result->n_containers, g)];
                 const uint64_t CS = uint64_t(d.chunk_size) * d.S;
                 const uint64_t o0 = d.out_off + k * CS;
                 const uint64_t o1 = o0 + (k + 1 == d.num_chunks ? uint64_t(d.last_len) * d.S : CS);
@@ -1028,21 +1111,31 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 
 }  // namespace
 
-int decode_ctas_per_sm() {
-    int blocks = 0;
-    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel<false>, kDecodeWarps * 32,
-                                                  smem);
-    return blocks;
+namespace {
+template <bool kPipe, int kKind>
+void launch_kind(const DecodeArgs& a, const DecodePipe& pp, int sms, cudaStream_t st) {
+    constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
+    const size_t smem = size_t(kDecodeWarps) * kWarpSmem;
+    static int per_sm = -1;  // same answer on every B200; computed once
+    if (per_sm < 0) {
+        int blocks = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_decode_kernel<kPipe, kKind>,
+                                                      kDecodeWarps * 32, smem);
+        per_sm = blocks > 0 ? blocks : 1;
+    }
+    plz_decode_kernel<kPipe, kKind><<<sms * per_sm, kDecodeWarps * 32, smem, st>>>(a, pp);
 }
+}  // namespace
 
 void launch_parse(const DecodeArgs& a, cudaStream_t st) {
     plz_parse_kernel<<<1, 256, 0, st>>>(a);
 }
 
-void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
-    plz_decode_kernel<false><<<grid, kDecodeWarps * 32, smem, st>>>(a, DecodePipe{});
+// the other widths first: in a one-width image (the usual case) that kernel
+// only skips containers, then the S = 2 kernel does the work
+void launch_decode(const DecodeArgs& a, int sms, cudaStream_t st) {
+    launch_kind<false, kKindOther>(a, DecodePipe{}, sms, st);
+    launch_kind<false, kKindS2>(a, DecodePipe{}, sms, st);
 }
 
 void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, uint64_t* res,
@@ -1050,9 +1143,9 @@ void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, u
     plz_range_kernel<<<1, 32, 0, st>>>(a, cb, ce, out, res);
 }
 
-void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st) {
-    const size_t smem = size_t(kDecodeWarps) * kFastWarpSmem;
-    plz_decode_kernel<true><<<grid, kDecodeWarps * 32, smem, st>>>(a, pp);
+void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int sms, cudaStream_t st) {
+    launch_kind<true, kKindOther>(a, pp, sms, st);
+    launch_kind<true, kKindS2>(a, pp, sms, st);
 }
 
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
@@ -1071,8 +1164,10 @@ void launch_decode_one(const DecodeOneArgs& a, cudaStream_t st) {
 
 void preload_decode_kernels() {
     for (const void* f : {reinterpret_cast<const void*>(plz_parse_kernel),
-                          reinterpret_cast<const void*>(plz_decode_kernel<false>),
-                          reinterpret_cast<const void*>(plz_decode_kernel<true>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<false, kKindOther>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<false, kKindS2>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<true, kKindOther>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<true, kKindS2>),
                           reinterpret_cast<const void*>(plz_chunk_detail_kernel),
                           reinterpret_cast<const void*>(plz_mono_detail_kernel),
                           reinterpret_cast<const void*>(plz_range_kernel),

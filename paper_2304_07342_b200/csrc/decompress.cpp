@@ -30,11 +30,9 @@ int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_
     a.mono_key = &m->mono_key;
     a.work = &m->work[2];
     launch_parse(a, st);
-    int per_sm = decode_ctas_per_sm();
-    if (per_sm < 1) per_sm = 1;
-    launch_decode(a, c->sms * per_sm, st);
+    launch_decode(a, c->sms, st);
     CK(cudaGetLastError());
-    c->last_launches = 2;
+    c->last_launches = 3;
     c->last_op = OP_DECOMPRESS;
     c->last_decode = a;
     return PLZGPU_OK;
@@ -242,16 +240,14 @@ int plzgpu_decompress_range(plzgpu_ctx* c, const void* img, uint64_t len, uint64
     if (ce > cb) {
         // the decode kernel over [cb, ce): work counter from cb, bound ce,
         // output addressed relative to the range's first byte
-        const uint32_t w0 = uint32_t(cb);
-        CK(cudaMemcpyAsync(&m->work[2], &w0, 4, cudaMemcpyHostToDevice, st));
+        const uint32_t w0[2] = {uint32_t(cb), uint32_t(cb)};  // both decode kernels' counters
+        CK(cudaMemcpyAsync(&m->work[2], w0, 8, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(&m->parse.total_chunks, &ce, 8, cudaMemcpyHostToDevice, st));
         a.out = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(d_out) - lo);
         a.out_cap = hi;
-        int per_sm = decode_ctas_per_sm();
-        if (per_sm < 1) per_sm = 1;
-        launch_decode(a, c->sms * per_sm, st);
+        launch_decode(a, c->sms, st);
         CK(cudaGetLastError());
-        c->last_launches = 3;
+        c->last_launches = 4;
         c->last_op = OP_DECOMPRESS;
         c->last_decode = a;
         bool grow = false;

@@ -303,9 +303,7 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
                             c->epoch, 0) != 0)
                 return 0;
     }
-    int per_sm = decode_ctas_per_sm();
-    if (per_sm < 1) per_sm = 1;
-    launch_decode_pipelined(a, pp, c->sms * per_sm, st);
+    launch_decode_pipelined(a, pp, c->sms, st);
     CK(cudaGetLastError());
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
@@ -324,7 +322,7 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     CK(cudaMemcpyAsync(h, m, sizeof(Meta), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaStreamSynchronize(c->copy_stream));
-    c->last_launches = 1;
+    c->last_launches = 2;
     c->last_op = OP_DECOMPRESS;
     c->last_decode = a;
     if (h->stalled || h->err_chunk != ~0ull || h->mono_key != ~0ull) return 0;

@@ -263,8 +263,10 @@ struct DecodePipe {
     uint64_t out_seg;
 };
 void launch_parse(const DecodeArgs& a, cudaStream_t st);
-void launch_decode(const DecodeArgs& a, int grid, cudaStream_t st);
-void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int grid, cudaStream_t st);
+// two launches (the S = 2 containers and the rest), each a persistent grid
+// sized for `sms` SMs; work counters a.work[0] and a.work[1]
+void launch_decode(const DecodeArgs& a, int sms, cudaStream_t st);
+void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int sms, cudaStream_t st);
 // chunk-range decode: res[0..2] = output range of chunks [cb, ce), total chunks;
 // writes the tails inside the range to out (relative to res[0])
 void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, uint64_t* res,
@@ -272,7 +274,6 @@ void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, u
 // re-decodes chunk *a.err_chunk and reports (TokenErr, chunk within container, token)
 void launch_chunk_detail(const DecodeArgs& a, uint32_t* code, uint64_t* chunk, uint64_t* token,
                          cudaStream_t st);
-int decode_ctas_per_sm();
 
 // Lazy module loading (the CUDA 12 default) loads a kernel at its first
 // launch, and that load waits for the device's running work: a launch queued
