@@ -13,15 +13,12 @@
 //
 // The kernel is a copy at HBM speed, so it is organised around memory
 // round trips:
-//  * offset tables: one thread per aligned 4-byte image word (coalesced
-//    32-bit stores; an entry straddling two words is funnel-shifted from its
-//    neighbours; the region's two edge words are written bytewise);
-//  * streams: one warp per chunk, its flag slice and payload slice copied as
-//    one job list — every source word the chunk needs is loaded before the
-//    first store (one DRAM round trip per chunk, not one per head / body /
-//    tail), realigned to the destination with funnel shifts and stored as
-//    aligned 128-bit words (edge words bytewise); the next chunk's prefixes
-//    are loaded while this chunk's data is in flight.
+//  * one warp per chunk: its two table entries (byte stores by 8 lanes), its
+//    flag slice and payload slice (warp_copy2: every source byte of both
+//    loaded before the first store, realigned 128-bit body stores); the next
+//    chunk's prefixes are loaded while this chunk's data is in flight;
+//  * the shard variant writes its table slices with one thread per aligned
+//    4-byte image word (coalesced; straddling entries funnel-shifted).
 // The header kernel (one thread per container) writes the 26-byte header,
 // the tail and the image length, and flags 4-byte table overflow
 // (scan.cpp:43-44).
@@ -33,81 +30,88 @@ namespace plzgpu {
 namespace {
 
 // ------------------------------------------------------------ stream copies
+// A chunk's flag slice and payload slice are copied by one warp as two jobs:
+// a byte head up to the destination's 16-byte alignment, 128-bit body words
+// realigned from two aligned source words (funnel shift; the shift is
+// uniform per job, so the select is a uniform branch), a byte tail.  Every
+// source byte of both jobs (up to 64 body words each) is loaded before the
+// first store: one DRAM round trip per chunk instead of one per head, body
+// iteration and tail of each slice.
 struct Job {
     uint8_t* dst;        // any alignment
     const uint8_t* src;  // 16-byte aligned; readable up to 16 bytes past len
-    uint32_t len;
+    uint32_t len, head, body, tail;
 };
 
-__device__ __forceinline__ uint32_t job_words(const Job& j) {
-    return j.len ? ((uint32_t(reinterpret_cast<uintptr_t>(j.dst) & 15u) + j.len + 15u) >> 4) : 0u;
+__device__ __forceinline__ Job make_job(uint8_t* dst, const uint8_t* src, uint32_t len) {
+    Job j;
+    j.dst = dst;
+    j.src = src;
+    j.len = len;
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(dst) & 15u);
+    j.head = min((16u - mis) & 15u, len);
+    j.body = (len - j.head) >> 4;
+    j.tail = len - j.head - 16u * j.body;
+    return j;
 }
 
-// 128-bit funnel shift: bytes [r, r + 16) of the 32-byte value (hi:lo), r in 0..15
-__device__ __forceinline__ uint4 funnel128(const uint4& lo, const uint4& hi, uint32_t r) {
-    const uint32_t q = r >> 2, s = 8u * (r & 3u);
+struct JobData {
+    uint32_t hb, tb;  // this lane's head / tail byte
+    uint4 a[2], b[2];  // body words lane and lane + 32: source words i and i + 1
+};
+
+__device__ __forceinline__ uint4 realign(const uint4& a, const uint4& b, uint32_t h) {
+    if (h == 0) return a;
     uint32_t y0, y1, y2, y3, y4;
-    switch (q) {
-        case 0: y0 = lo.x; y1 = lo.y; y2 = lo.z; y3 = lo.w; y4 = hi.x; break;
-        case 1: y0 = lo.y; y1 = lo.z; y2 = lo.w; y3 = hi.x; y4 = hi.y; break;
-        case 2: y0 = lo.z; y1 = lo.w; y2 = hi.x; y3 = hi.y; y4 = hi.z; break;
-        default: y0 = lo.w; y1 = hi.x; y2 = hi.y; y3 = hi.z; y4 = hi.w; break;
+    switch (h >> 2) {
+        case 0: y0 = a.x; y1 = a.y; y2 = a.z; y3 = a.w; y4 = b.x; break;
+        case 1: y0 = a.y; y1 = a.z; y2 = a.w; y3 = b.x; y4 = b.y; break;
+        case 2: y0 = a.z; y1 = a.w; y2 = b.x; y3 = b.y; y4 = b.z; break;
+        default: y0 = a.w; y1 = b.x; y2 = b.y; y3 = b.z; y4 = b.w; break;
     }
+    const uint32_t r = 8u * (h & 3u);
     uint4 o;
-    o.x = __funnelshift_r(y0, y1, s);
-    o.y = __funnelshift_r(y1, y2, s);
-    o.z = __funnelshift_r(y2, y3, s);
-    o.w = __funnelshift_r(y3, y4, s);
+    o.x = __funnelshift_r(y0, y1, r);
+    o.y = __funnelshift_r(y1, y2, r);
+    o.z = __funnelshift_r(y2, y3, r);
+    o.w = __funnelshift_r(y3, y4, r);
     return o;
 }
 
-// Word w of a job: the aligned 16-byte destination word W0 + 16w (W0 = dst
-// rounded down); its bytes come from source bytes [16w - m, 16w - m + 16),
-// m = dst & 15, i.e. source words w - 1 and w (word -1 reads as zeros: its
-// bytes lie before dst and are never stored).  Only the source words are
-// kept between the load and the store (registers: 4 words per lane).
-__device__ __forceinline__ void load_word(const Job& j, uint32_t w, uint4& lo, uint4& hi) {
-    const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(j.dst) & 15u);
+__device__ __forceinline__ void load_job(const Job& j, JobData& d, uint32_t lane) {
     const uint4* s16 = reinterpret_cast<const uint4*>(j.src);
-    hi = __ldg(s16 + w);
-    lo = (m && w) ? __ldg(s16 + w - 1) : make_uint4(0, 0, 0, 0);
-}
-
-__device__ __forceinline__ void store_word(const Job& j, uint32_t w, const uint4& lo,
-                                           const uint4& hi) {
-    const uint32_t m = uint32_t(reinterpret_cast<uintptr_t>(j.dst) & 15u);
-    uint8_t* at = j.dst - m + 16u * w;
-    const int32_t b0 = w == 0 ? int32_t(m) : 0;
-    const int32_t end = int32_t(m + j.len) - int32_t(16u * w);
-    const int32_t b1 = end < 16 ? end : 16;
-    const uint4 v = m ? funnel128(lo, hi, 16u - m) : hi;
-    if (b0 == 0 && b1 == 16) {
-        *reinterpret_cast<uint4*>(at) = v;
-        return;
-    }
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+    d.hb = lane < j.head ? j.src[lane] : 0u;
+    d.tb = lane < j.tail ? j.src[j.head + 16u * j.body + lane] : 0u;
 #pragma unroll
-    for (int b = 0; b < 16; ++b)
-        if (b >= b0 && b < b1) at[b] = uint8_t(wv[b >> 2] >> (8 * (b & 3)));
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t i = lane + 32u * u;
+        if (i < j.body) {
+            d.a[u] = __ldg(s16 + i);
+            if (j.head) d.b[u] = __ldg(s16 + i + 1);
+        }
+    }
 }
 
-// One warp copies two jobs (a chunk's flag and payload slices): up to 4
-// words per lane per round, all of a round's loads before its stores.
+__device__ __forceinline__ void store_job(const Job& j, const JobData& d, uint32_t lane) {
+    if (lane < j.head) j.dst[lane] = uint8_t(d.hb);
+    uint4* d16 = reinterpret_cast<uint4*>(j.dst + j.head);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+        const uint32_t i = lane + 32u * u;
+        if (i < j.body) d16[i] = realign(d.a[u], d.b[u], j.head);
+    }
+    const uint4* s16 = reinterpret_cast<const uint4*>(j.src);
+    for (uint32_t i = lane + 64u; i < j.body; i += 32u)  // bodies past 1 KiB
+        d16[i] = realign(__ldg(s16 + i), j.head ? __ldg(s16 + i + 1) : make_uint4(0, 0, 0, 0), j.head);
+    if (lane < j.tail) j.dst[j.head + 16u * j.body + lane] = uint8_t(d.tb);
+}
+
 __device__ __forceinline__ void warp_copy2(const Job& j0, const Job& j1, uint32_t lane) {
-    const uint32_t n0 = job_words(j0), n = n0 + job_words(j1);
-    for (uint32_t base = 0; base < n; base += 128) {
-        uint4 lo[4], hi[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t i = base + lane + 32u * u;
-            if (i < n) load_word(i < n0 ? j0 : j1, i < n0 ? i : i - n0, lo[u], hi[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const uint32_t i = base + lane + 32u * u;
-            if (i < n) store_word(i < n0 ? j0 : j1, i < n0 ? i : i - n0, lo[u], hi[u]);
-        }
-    }
+    JobData d0, d1;
+    load_job(j0, d0, lane);
+    load_job(j1, d1, lane);
+    store_job(j0, d0, lane);
+    store_job(j1, d1, lane);
 }
 
 // ------------------------------------------------------------ offset tables
@@ -160,38 +164,19 @@ __device__ __forceinline__ uint64_t container_start(const AssembleArgs& a, uint6
     return 26u * j + 8u * (g0 + j) + a.P64[g0] + a.F64[g0];
 }
 
-__global__ void __launch_bounds__(256, 3) plz_assemble_kernel(AssembleArgs a) {
+__global__ void __launch_bounds__(128) plz_assemble_kernel(AssembleArgs a) {
     const uint32_t lane = lane_id();
     const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
-    // ---- offset tables: both tables of container j are one region of
-    // 2(n+1) entries at image byte img0 + 26
-    {
-        const uint64_t stride = 2 * (a.cpb + 1) + 1;  // words per container, at most
-        const uint64_t total = (j_hi - a.j_lo) * stride;
-        for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-             idx += uint64_t(gridDim.x) * blockDim.x) {
-            const uint64_t j = a.j_lo + idx / stride, wi = idx % stride;
-            const uint64_t g0 = j * a.cpb;
-            const uint64_t n = (j + 1 == a.n_blocks) ? a.n_chunks - g0 : a.cpb;
-            uint8_t* region = a.img + container_start(a, j, g0) + 26;
-            if (wi >= table_words(region, 2 * (n + 1))) continue;
-            const uint64_t pb = a.P64[g0], fb = a.F64[g0];
-            table_word(region, 2 * (n + 1), wi, [&](uint64_t e) {
-                return e <= n ? uint32_t(a.P64[g0 + e] - pb) : uint32_t(a.F64[g0 + e - (n + 1)] - fb);
-            });
-        }
-    }
-    // ---- streams: warp per chunk
     const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
     const uint64_t g_lo = a.j_lo * a.cpb;
     const uint64_t g_hi = min(a.n_chunks, j_hi * a.cpb);
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     uint64_t g = g_lo + uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (g >= g_hi) return;
-    // per-chunk prefixes, loaded one chunk ahead
+    // per-chunk prefixes and sizes, loaded one chunk ahead
     uint64_t pg = a.P64[g], fg = a.F64[g];
     uint32_t ps = a.psize[g], fs = a.fsize[g];
-    uint64_t cj = ~0ull, streams = 0, pb = 0, fb = 0, ftot = 0;
+    uint64_t cj = ~0ull, g0 = 0, n = 0, tabs = 0, pb = 0, fb = 0, ftot = 0;
     for (; g < g_hi; g += warps) {
         const uint64_t gn = g + warps;
         uint64_t pg_n = 0, fg_n = 0;
@@ -203,16 +188,30 @@ __global__ void __launch_bounds__(256, 3) plz_assemble_kernel(AssembleArgs a) {
             fs_n = a.fsize[gn];
         }
         const Geo c = locate(a, g);
-        if (c.j != cj) {
+        if (c.j != cj) {  // container constants, cached while the warp stays in it
             cj = c.j;
-            pb = a.P64[c.g0];
-            fb = a.F64[c.g0];
-            ftot = a.F64[c.g0 + c.n] - fb;
-            streams = container_start(a, c.j, c.g0) + 26 + 8 * (c.n + 1);
+            g0 = c.g0;
+            n = c.n;
+            pb = a.P64[g0];
+            fb = a.F64[g0];
+            ftot = a.F64[g0 + n] - fb;
+            tabs = container_start(a, cj, g0) + 26;
         }
-        const Job jf{a.img + streams + (fg - fb), a.flag_slots + g * (C / 8), fs};
-        const Job jp{a.img + streams + ftot + (pg - pb), a.pay_slots + g * C * S, ps};
-        warp_copy2(jf, jp, lane);
+        const uint64_t pk = pg - pb, fk = fg - fb, k = g - g0;
+        const uint64_t streams = tabs + 8 * (n + 1);
+        const Job jf = make_job(a.img + streams + fk, a.flag_slots + g * (C / 8), fs);
+        const Job jp = make_job(a.img + streams + ftot + pk, a.pay_slots + g * C * S, ps);
+        JobData df, dp;
+        load_job(jf, df, lane);
+        load_job(jp, dp, lane);
+        // table entries k (the header kernel writes entry n)
+        if (lane < 4) {
+            a.img[tabs + 4 * k + lane] = uint8_t(pk >> (8 * lane));
+        } else if (lane < 8) {
+            a.img[tabs + 4 * (n + 1) + 4 * k + (lane - 4)] = uint8_t(fk >> (8 * (lane - 4)));
+        }
+        store_job(jf, df, lane);
+        store_job(jp, dp, lane);
         pg = pg_n;
         fg = fg_n;
         ps = ps_n;
@@ -311,8 +310,8 @@ __global__ void __launch_bounds__(256, 4) plz_shard_assemble_kernel(ShardAssembl
         const uint64_t lp = a.P64[g] - a.P64[d.g_lo], lf = a.F64[g] - a.F64[d.g_lo];
         const uint64_t pk = d.p_base + lp, fk = d.f_base + lf;
         if (lane == 0 && (pk > 0xffffffffull || fk > 0xffffffffull)) atomicExch(a.overflow, 1u);
-        const Job jf{a.out + d.seg_flags + lf, a.flag_slots + g * (C / 8), a.fsize[g]};
-        const Job jp{a.out + d.seg_pay + lp, a.pay_slots + g * C * S, a.psize[g]};
+        const Job jf = make_job(a.out + d.seg_flags + lf, a.flag_slots + g * (C / 8), a.fsize[g]);
+        const Job jp = make_job(a.out + d.seg_pay + lp, a.pay_slots + g * C * S, a.psize[g]);
         warp_copy2(jf, jp, lane);
     }
 }
@@ -362,9 +361,9 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     const uint64_t g_lo = a.j_lo * a.cpb;
     const uint64_t g_hi = a.j_hi ? std::min(a.n_chunks, a.j_hi * a.cpb) : a.n_chunks;
     const uint64_t warps_needed = g_hi - g_lo;
-    uint64_t blocks = (warps_needed + 7) / 8;
-    if (blocks > 148ull * 8) blocks = 148ull * 8;
-    plz_assemble_kernel<<<unsigned(blocks), 256, 0, st>>>(a);
+    uint64_t blocks = (warps_needed + 3) / 4;
+    if (blocks > 148ull * 10) blocks = 148ull * 10;
+    plz_assemble_kernel<<<unsigned(blocks), 128, 0, st>>>(a);
 }
 
 void launch_headers(const AssembleArgs& a, cudaStream_t st) {

@@ -73,7 +73,7 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
                             c->copy_stream})
         if (sx) cudaStreamDestroy(sx);
     for (cudaEvent_t ev : {c->side_ev[0], c->side_ev[1], c->asm_ev[0], c->asm_ev[1],
-                           c->bounce_ev[0], c->bounce_ev[1]})
+                           c->bounce_ev[0], c->bounce_ev[1], c->bounce_ev[2], c->order_ev})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : c->cont_ev)
         if (ev) cudaEventDestroy(ev);

@@ -38,13 +38,12 @@ constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSme
 // (kDecodeSmem bytes), token table (one byte per token: a pointer's offset,
 // 0 for a literal; kFastTokens entries — a chunk with more flag bits than
 // that takes decode_chunk_smem), wave table (per 32 output positions:
-// token-start bitmap + address of the token before the wave, bit 31 =
-// in-wave sources possible), chase bits (one per wave).
+// token-start bitmap + address of the token before the wave; read two
+// entries at a time, so one spare entry).
 constexpr uint32_t kFastTokens = 2048;
 constexpr uint32_t kFastPtab = kDecodeSmem;
 constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
-constexpr uint32_t kFastChase = kFastMeta + kDecodeSmem / 4;
-constexpr uint32_t kFastWarpSmem = kFastChase + kDecodeSmem / 256;
+constexpr uint32_t kFastWarpSmem = kFastMeta + kDecodeSmem / 4 + 16;
 static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
 constexpr bool kUseFast = true;
 constexpr uint32_t kMainWarpSmem = kUseFast ? kFastWarpSmem : kDecodeWarpSmem;
@@ -421,14 +420,13 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
 //     bytes as 5 aligned words, other widths byte by byte), so one warp scan
 //     per 256 tokens places them.  Literals go straight to the stage, every
 //     token start is set in its wave's start bitmap and its offset (0 for a
-//     literal) lands in the token table; a pointer whose source may lie in its
-//     own 32-position wave (off < 32) marks that wave.
+//     literal) lands in the token table.
 //  B. waves of 32 output positions in order: one shared load of the wave's
 //     bitmap + token base, a popcount gives each lane its covering token, one
 //     byte load its offset, and the lane copies out[q - off] (a literal
-//     position copies onto itself).  In a marked wave the lanes first check
-//     whether any source is an in-wave pointer position and only then resolve
-//     by pointer jumping over the lanes' sources.
+//     position copies onto itself).  One shuffle tells whether any source is
+//     an in-wave pointer position (not final yet); only then are the sources
+//     resolved by pointer jumping over the lanes.
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -445,13 +443,11 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                                   uint8_t* wsm, uint32_t lane) {
     constexpr uint32_t FULL = 0xffffffffu;
     uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);  // pairs {starts, base}
-    uint32_t* chase = reinterpret_cast<uint32_t*>(wsm + kFastChase);
     const uint32_t s_stage = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
     const uint32_t s_ptab = s_stage + kFastPtab;
     const uint32_t s_meta = s_stage + kFastMeta;
     const uint32_t nwv = (L + 31u) >> 5;
     for (uint32_t w = lane; w < nwv; w += 32) meta[2 * w] = 0u;
-    if (lane < kDecodeSmem / 1024) chase[lane] = 0u;
     __syncwarp();
     // ---- phase A
     uint32_t written = 0, in = 0, tbase = 0, T = 0, in_end = 0;
@@ -534,15 +530,6 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                 if (!bit) sts_sym<S>(s_stage + pos * S, S == 4 ? fld : fld & ((1u << (8 * S)) - 1u));
                 atomicOr(&meta[2 * (pos >> 5)], 1u << (pos & 31u));
                 asm volatile("st.shared.u8 [%0], %1;" ::"r"(s_ptab + t), "r"(off));
-                if (bit && off < 32u) {
-                    const uint32_t w0 = pos >> 5, w1 = (pos + len - 1u) >> 5;
-                    if (len <= off) {
-                        atomicOr(&chase[w0 >> 5], 1u << (w0 & 31u));
-                        if (w1 != w0) atomicOr(&chase[w1 >> 5], 1u << (w1 & 31u));
-                    } else {  // replicating pointer (len > off): every wave it covers
-                        for (uint32_t w = w0; w <= w1; ++w) atomicOr(&chase[w >> 5], 1u << (w & 31u));
-                    }
-                }
                 ++nreach;
                 o_reach = o + sz;
             }
@@ -571,40 +558,43 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         const uint32_t w = w0 + lane;
         const uint32_t c = w < nwv ? __popc(meta[2 * w]) : 0u;
         const uint32_t inc = warp_incl_scan_u32(c, lane);
-        if (w < nwv)
-            meta[2 * w + 1] = (s_ptab + carry + inc - c - 1u) | (((chase[w >> 5] >> (w & 31u)) & 1u) << 31);
+        if (w < nwv) meta[2 * w + 1] = s_ptab + carry + inc - c - 1u;
         carry += __shfl_sync(FULL, inc, 31);
     }
     __syncwarp();
-    // ---- phase B
+    // ---- phase B: two waves per step (one 16-byte load of both table
+    // entries, both lookups before the first copy)
     const uint32_t upto = (2u << lane) - 1u;
     uint32_t a_q = s_stage + lane * uint32_t(S);
-    for (uint32_t w = 0; w < nwv; ++w) {
-        uint32_t st, tb;
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(st), "=r"(tb) : "r"(s_meta + 8u * w));
-        const uint32_t off = lds_u8((tb & 0x7fffffffu) + __popc(st & upto));
-        uint32_t val;
-        if (tb & 0x80000000u) {  // in-wave sources possible
-            const int wb = int(w << 5);
-            int src = wb + int(lane) - int(off);
-            // is any lane's source an in-wave POINTER position (not yet final)?
-            const uint32_t soff = __shfl_sync(FULL, off, uint32_t(src) & 31u);
-            if (__any_sync(FULL, src >= wb && soff != 0u)) {
-                bool more;
-                do {  // pointer jumping over the lanes' sources
-                    const bool inw = src >= wb;
-                    const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
-                    more = inw && s2 != src;
-                    src = inw ? s2 : src;
-                } while (__any_sync(FULL, more));
-            }
-            val = lds_sym<S>(s_stage + uint32_t(src) * S);
-        } else {
-            val = lds_sym<S>(a_q - off * S);
+    auto wave = [&](uint32_t w, uint32_t off) {
+        const int wb = int(w << 5);
+        int src = wb + int(lane) - int(off);
+        // a source inside the wave that is a pointer position is not final
+        // yet: resolve by pointer jumping over the lanes' sources (a literal
+        // position is its own source)
+        const uint32_t soff = __shfl_sync(FULL, off, uint32_t(src) & 31u);
+        if (__any_sync(FULL, src >= wb && soff != 0u)) {
+            bool more;
+            do {
+                const bool inw = src >= wb;
+                const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
+                more = inw && s2 != src;
+                src = inw ? s2 : src;
+            } while (__any_sync(FULL, more));
         }
-        sts_sym<S>(a_q, val);
+        sts_sym<S>(a_q, lds_sym<S>(s_stage + uint32_t(src) * S));
         a_q += 32u * S;
         __syncwarp();
+    };
+    for (uint32_t w = 0; w < nwv; w += 2) {
+        uint32_t st0, tb0, st1, tb1;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(st0), "=r"(tb0), "=r"(st1), "=r"(tb1) : "r"(s_meta + 8u * w));
+        const uint32_t off0 = lds_u8(tb0 + __popc(st0 & upto));
+        const bool two = w + 1 < nwv;
+        const uint32_t off1 = two ? lds_u8(tb1 + __popc(st1 & upto)) : 0u;
+        wave(w, off0);
+        if (two) wave(w + 1, off1);
     }
     return true;
 }

@@ -194,6 +194,8 @@ const PipelineConfig& pipeline_config() {
         c.dseg_group = env_u64("PLZGPU_DSEG_GROUP", c.dseg_group, 1, 1);
         c.dseg_group_out = env_u64("PLZGPU_DSEG_GROUP_OUT", c.dseg_group, 1, 1);
         c.pageable_stage = env_u64("PLZGPU_PAGEABLE_MB", c.pageable_stage, MB, MB);
+        c.pageable_min = env_u64("PLZGPU_PAGEABLE_MIN_MB", c.pageable_min, MB, 0);
+        c.copy_threads = int(env_u64("PLZGPU_COPY_THREADS", 0, 1, 0));
         return c;
     }();
     return cfg;

@@ -83,7 +83,9 @@ struct PipelineConfig {
     uint64_t dseg_lead = 1;           // PLZGPU_DSEG_LEAD: single-segment transfers first
     uint64_t dseg_group = 1;          // PLZGPU_DSEG_GROUP: segments per later H2D transfer
     uint64_t dseg_group_out = 1;      // PLZGPU_DSEG_GROUP_OUT: segments per later D2H transfer
-    uint64_t pageable_stage = 64u << 20;  // PLZGPU_PAGEABLE_MB: pinned bounce buffer per direction
+    uint64_t pageable_stage = 64u << 20;  // PLZGPU_PAGEABLE_MB: one pinned bounce slot
+    uint64_t pageable_min = 64u << 20;    // PLZGPU_PAGEABLE_MIN_MB: staged copies from this size on
+    int copy_threads = 0;                 // PLZGPU_COPY_THREADS: host copy workers (0: cores - 1, <= 15)
 };
 const PipelineConfig& pipeline_config();
 
@@ -209,10 +211,11 @@ struct plzgpu_ctx {
     unsigned long long* enc_hist = nullptr;  // set while enqueueing a histogram encode
     plzhost::DevBuf hist, table;
     plzhost::DevBuf qtiles, qoff, qdelta;  // cuSZ quantizer scratch
-    // pageable host buffers: pinned bounce buffers (two per direction)
-    uint8_t* bounce[2] = {nullptr, nullptr};
+    // pageable host buffers: pinned bounce slots (staged copies)
+    uint8_t* bounce[3] = {nullptr, nullptr, nullptr};
     size_t bounce_cap = 0;
-    cudaEvent_t bounce_ev[2] = {nullptr, nullptr};
+    cudaEvent_t bounce_ev[3] = {nullptr, nullptr, nullptr};
+    cudaEvent_t order_ev = nullptr;
     // last plzgpu_shard_encode: the range and its per-container local totals
     uint64_t sh_begin = 0, sh_end = 0, sh_n = 0;
     plzgpu_params sh_params{};
@@ -244,13 +247,23 @@ int compress_host_input(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* in
                         cudaStream_t st, plzgpu_error* err);
 int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, uint8_t* out,
                              uint64_t cap, uint64_t* out_len, cudaStream_t st, plzgpu_error* err);
-// Pageable host buffer <-> device through the context's pinned bounce
-// buffers, double-buffered on the copy stream (a plain cudaMemcpy of
-// pageable memory stages through the driver's own small buffers).
-int h2d_pageable(plzgpu_ctx* c, uint8_t* d_dst, const uint8_t* h_src, uint64_t n, cudaStream_t st,
+// Pageable host memory <-> device through the context's pinned bounce slots:
+// a process-wide pool of host threads copies between the caller's pages and
+// one slot while the copy engine moves another (a plain cudaMemcpy of
+// pageable memory goes through the driver's own single-threaded staging,
+// ~10 GB/s).  Both run on c->copy_stream after the work already on `after`.
+//  h2d: returns once every DMA is enqueued; with `ready`, each slot's DMA is
+//       followed by the ready flags (= `epoch`) of the seg_bytes segments it
+//       completes, for kernels already waiting on them.
+//  d2h: returns once h_dst holds the bytes.
+bool use_staged(const void* host_ptr, uint64_t n);  // pageable and large enough
+int h2d_pageable(plzgpu_ctx* c, uint8_t* d_dst, const uint8_t* h_src, uint64_t n,
+                 cudaStream_t after, const uint32_t* ready, uint64_t seg_bytes, uint32_t epoch,
                  plzgpu_error* err);
-int d2h_pageable(plzgpu_ctx* c, uint8_t* h_dst, const uint8_t* d_src, uint64_t n, cudaStream_t st,
-                 plzgpu_error* err);
+int d2h_pageable(plzgpu_ctx* c, uint8_t* h_dst, const uint8_t* d_src, uint64_t n,
+                 cudaStream_t after, plzgpu_error* err);
+// memcpy between host buffers split over the copy pool's threads
+void pool_memcpy(void* dst, const void* src, size_t n);
 // decompress.cpp
 int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_t* d_out,
                        uint64_t cap, uint64_t* d_out_len, cudaStream_t st, plzgpu_error* err);
