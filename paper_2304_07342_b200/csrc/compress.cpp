@@ -309,10 +309,15 @@ int plzgpu_compress(plzgpu_ctx* c, const plzgpu_params* params, const void* in, 
         return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex,
                        "output buffer too small: need %llu bytes", (unsigned long long)h->img_len);
     if (!direct) {
-        CK(cudaMemcpyAsync(out, img, h->img_len,
-                           is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                           st));
-        CK(cudaStreamSynchronize(st));
+        if (use_staged(out, h->img_len)) {
+            rc = d2h_pageable(c, static_cast<uint8_t*>(out), img, h->img_len, st, err);
+            if (rc) return rc;
+        } else {
+            CK(cudaMemcpyAsync(out, img, h->img_len,
+                               is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                               st));
+            CK(cudaStreamSynchronize(st));
+        }
     }
     *out_len = h->img_len;
     if (stats) {

@@ -571,17 +571,15 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         int src = wb + int(lane) - int(off);
         // a source inside the wave that is a pointer position is not final
         // yet: resolve by pointer jumping over the lanes' sources (a literal
-        // position is its own source)
-        const uint32_t soff = __shfl_sync(FULL, off, uint32_t(src) & 31u);
-        if (__any_sync(FULL, src >= wb && soff != 0u)) {
-            bool more;
-            do {
-                const bool inw = src >= wb;
-                const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
-                more = inw && s2 != src;
-                src = inw ? s2 : src;
-            } while (__any_sync(FULL, more));
-        }
+        // position is its own source, so a lane whose source lane copies
+        // from elsewhere takes that source; the first step is the check)
+        bool more;
+        do {
+            const bool inw = src >= wb;
+            const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
+            more = inw && s2 != src;
+            src = inw ? s2 : src;
+        } while (__any_sync(FULL, more));
         sts_sym<S>(a_q, lds_sym<S>(s_stage + uint32_t(src) * S));
         a_q += 32u * S;
         __syncwarp();

@@ -130,7 +130,13 @@ int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, u
     clear_err(err);  // the resident path below reports any error
     if (!is_device_ptr(img)) {
         CK(c->img.ensure(len));
-        CK(cudaMemcpyAsync(c->img.p, img, len, cudaMemcpyHostToDevice, st));
+        if (use_staged(img, len)) {
+            const int rc = h2d_pageable(c, c->img.as<uint8_t>(), static_cast<const uint8_t*>(img),
+                                        len, st, true, nullptr, 0, 0, err);
+            if (rc) return rc;
+        } else {
+            CK(cudaMemcpyAsync(c->img.p, img, len, cudaMemcpyHostToDevice, st));
+        }
         d_img = c->img.as<uint8_t>();
     }
     const bool direct = is_device_ptr(out) && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
@@ -153,10 +159,15 @@ int plzgpu_decompress(plzgpu_ctx* c, const void* img, uint64_t len, void* out, u
     CK(cudaStreamSynchronize(st));
     const uint64_t total = h.parse.total_out;
     if (!direct && total) {
-        CK(cudaMemcpyAsync(out, d_out, total,
-                           is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                           st));
-        CK(cudaStreamSynchronize(st));
+        if (use_staged(out, total)) {
+            const int rc = d2h_pageable(c, static_cast<uint8_t*>(out), d_out, total, st, err);
+            if (rc) return rc;
+        } else {
+            CK(cudaMemcpyAsync(out, d_out, total,
+                               is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                               st));
+            CK(cudaStreamSynchronize(st));
+        }
     }
     *out_len = total;
     return PLZGPU_OK;

@@ -247,21 +247,23 @@ int compress_host_input(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* in
                         cudaStream_t st, plzgpu_error* err);
 int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, uint8_t* out,
                              uint64_t cap, uint64_t* out_len, cudaStream_t st, plzgpu_error* err);
-// Pageable host memory <-> device through the context's pinned bounce slots:
-// a process-wide pool of host threads copies between the caller's pages and
-// one slot while the copy engine moves another (a plain cudaMemcpy of
-// pageable memory goes through the driver's own single-threaded staging,
-// ~10 GB/s).  Both run on c->copy_stream after the work already on `after`.
-//  h2d: returns once every DMA is enqueued; with `ready`, each slot's DMA is
-//       followed by the ready flags (= `epoch`) of the seg_bytes segments it
-//       completes, for kernels already waiting on them.
-//  d2h: returns once h_dst holds the bytes.
+// Pageable host memory <-> device through the context's pinned bounce slots
+// (staging.cpp): a process-wide pool of host threads copies between the
+// caller's pages and one slot while the copy engine moves another (a plain
+// cudaMemcpy of pageable memory goes through the driver's own
+// single-threaded staging, ~10 GB/s).  The DMAs run on c->copy_stream.
+//  h2d: after_st orders the copies after the work already on st.  With
+//       `ready`, each slot's DMA is followed by the ready flags (= epoch) of
+//       the seg_bytes segments it completes, for kernels already waiting on
+//       them; without, st waits for the copies.  Returns once every DMA is
+//       enqueued.
+//  d2h: after the work on st; returns once h_dst holds the bytes.
 bool use_staged(const void* host_ptr, uint64_t n);  // pageable and large enough
 int h2d_pageable(plzgpu_ctx* c, uint8_t* d_dst, const uint8_t* h_src, uint64_t n,
-                 cudaStream_t after, const uint32_t* ready, uint64_t seg_bytes, uint32_t epoch,
+                 cudaStream_t st, bool after_st, const uint32_t* ready, uint64_t seg_bytes,
+                 uint32_t epoch, plzgpu_error* err);
+int d2h_pageable(plzgpu_ctx* c, uint8_t* h_dst, const uint8_t* d_src, uint64_t n, cudaStream_t st,
                  plzgpu_error* err);
-int d2h_pageable(plzgpu_ctx* c, uint8_t* h_dst, const uint8_t* d_src, uint64_t n,
-                 cudaStream_t after, plzgpu_error* err);
 // memcpy between host buffers split over the copy pool's threads
 void pool_memcpy(void* dst, const void* src, size_t n);
 // decompress.cpp

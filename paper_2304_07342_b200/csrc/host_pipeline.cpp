@@ -139,7 +139,13 @@ int compress_host_input(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* in
                        : enqueue_compress(c, p, d_in, n, img, &m->img_len, st, err);
     c->pipe_ready = nullptr;
     if (rc) return rc;
-    if (!pinned_in && (rc = enqueue_copies())) return rc;
+    if (!pinned_in) {  // pageable: staged by the copy pool when large
+        rc = use_staged(in, n) ? h2d_pageable(c, c->in.as<uint8_t>(), in, n, st, false,
+                                              c->ready.as<uint32_t>(), seg_chunks * chunk_bytes,
+                                              c->epoch, err)
+                               : enqueue_copies();
+        if (rc) return rc;
+    }
     if (!per_container || cfg.asm_mapped) return PLZGPU_OK;
     // each container's image range is known once its scan is done (global
     // stream prefixes P64 / F64 at its first and last chunk): read the four
@@ -291,9 +297,11 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     pp.in_seg = seg_in;
     pp.out_done = c->done.as<uint32_t>();
     pp.out_seg = seg_out;
-    // the image up, segment by segment, after the flags' reset above
+    // the image up, segment by segment, after the flags' reset above (a
+    // large pageable image: staged by the copy pool, after the launch below)
+    const bool staged = use_staged(img, len);
     CK(cudaStreamWaitEvent(c->copy_stream, c->asm_ev[0], 0));
-    for (uint64_t sg = 0; sg < nseg_in;) {
+    for (uint64_t sg = staged ? nseg_in : 0; sg < nseg_in;) {
         const uint64_t s_end = std::min(nseg_in, sg + (sg < kLead ? 1 : kGroup));
         const uint64_t lo = sg * seg_in, hi = std::min(len, s_end * seg_in);
         CK(cudaMemcpyAsync(c->img.as<uint8_t>() + lo, img + lo, hi - lo, cudaMemcpyHostToDevice,
@@ -305,6 +313,11 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     }
     launch_decode_pipelined(a, pp, c->sms, st);
     CK(cudaGetLastError());
+    if (staged) {
+        const int rc = h2d_pageable(c, c->img.as<uint8_t>(), img, len, st, false, pp.in_ready, seg_in,
+                                    c->epoch, err);
+        if (rc) return rc;
+    }
     // the output down, each segment once its decoded bytes are counted
     CK(cudaStreamWaitEvent(c->asm_stream, c->asm_ev[0], 0));
     for (uint64_t sg = 0; sg < nseg_out;) {
