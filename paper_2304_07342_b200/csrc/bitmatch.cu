@@ -170,10 +170,11 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
     using T = typename Sym<S>::T;
     constexpr uint32_t kEmpty = 0xffffffffu;
     constexpr int H = 2 * MAXS;  // table slots: load factor <= 1/2
-    constexpr int HB = MAXS == 16 ? 5 : MAXS == 32 ? 6 : 7;
+    constexpr int HB = MAXS == 4 ? 3 : MAXS == 16 ? 5 : MAXS == 32 ? 6 : 7;
     static_assert((1 << HB) == H, "hash size");
 #pragma unroll
-    for (int i = 0; i < H / 32; ++i) tbl[i * 32 + lane] = make_uint2(0u, kEmpty);
+    for (int i = 0; i < (H + 31) / 32; ++i)
+        if (H >= 32 || static_cast<int>(lane) < H) tbl[i * 32 + lane] = make_uint2(0u, kEmpty);
     __syncwarp();
     const T* rs = reinterpret_cast<const T*>(raw);
     D = 0;
@@ -224,14 +225,13 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
     return true;
 }
 
-// Which later pass takes a chunk the first pass could not hold: 0 if it has
-// at most kBmMaxSymsMid distinct symbols, 1 if at most kBmMaxSymsWide, else
-// 2.  Counts exactly (up to 65) from the input in global memory — the first
-// pass has overwritten part of its staged copy with ids.  Lane d % 32 keeps
-// distinct symbol d in tab[d / 32]; each word's new values are appended one
-// distinct value at a time.
+// The chunk's number of distinct symbols, counted exactly up to
+// kBmMaxSymsWide + 1, from the input in global memory (the first pass has
+// overwritten part of its staged copy with ids).  Lane d % 32 keeps distinct
+// symbol d in tab[d / 32]; each word's new values are appended one distinct
+// value at a time.
 template <int S>
-__device__ __noinline__ int classify_alphabet(const uint8_t* src, int n, uint32_t lane) {
+__device__ __noinline__ int count_alphabet(const uint8_t* src, int n, uint32_t lane) {
     uint32_t tab[2] = {0u, 0u};
     int D = 0;
     for (int wi = 0; wi * 32 < n && D <= kBmMaxSymsWide; ++wi) {
@@ -261,7 +261,7 @@ __device__ __noinline__ int classify_alphabet(const uint8_t* src, int n, uint32_
             }
         }
     }
-    return D <= kBmMaxSymsMid ? 0 : D <= kBmMaxSymsWide ? 1 : 2;
+    return D;
 }
 
 // Pass 2: occurrence rows from the ids.  Lanes holding equal ids form one
@@ -339,8 +339,11 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
         uint32_t tab[(MAXS + 31) / 32];
         if (!rename_symbols<S, MAXS>(raw, n, tbl, lane, D, tab)) {
             // too many distinct symbols: the wide-cell pass takes this chunk
-            const int cls = (MAXS == kBmMaxSyms && a.classify)
-                                ? classify_alphabet<S>(a.in + ck * uint64_t(C) * S, n, lane) : 0;
+            int cls = 0;
+            if (MAXS == kBmMaxSyms && a.classify) {
+                const int D2 = count_alphabet<S>(a.in + ck * uint64_t(C) * S, n, lane);
+                cls = D2 <= kBmMaxSymsMid ? 0 : D2 <= kBmMaxSymsWide ? 1 : 2;
+            }
             if (lane == 0) a.fb_list[cls][atomicAdd(a.fb_count[cls], 1u)] = uint32_t(ck);
             __syncwarp();
             continue;
@@ -474,8 +477,25 @@ const void* bitmatch_fn_m(int S, int nw) {
     return bitmatch_fn_s<4, MAXS>(nw);
 }
 
+// Latency mode's classification: one warp per chunk (grid-stride).
+template <int S>
+__global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_t* lists,
+                                                           uint64_t stride, uint32_t* counts) {
+    const uint32_t lane = lane_id();
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    for (uint64_t ck = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+         ck < a.n_chunks; ck += warps) {
+        const int n = (ck + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : a.C;
+        const int D = count_alphabet<S>(a.in + ck * uint64_t(a.C) * S, n, lane);
+        const int k = D <= kBmMaxSymsTiny ? 0 : D <= kBmMaxSyms ? 1 : D <= kBmMaxSymsMid ? 2
+                    : D <= kBmMaxSymsWide ? 3 : 4;
+        if (lane == 0) lists[uint64_t(k) * stride + atomicAdd(&counts[k], 1u)] = uint32_t(ck);
+    }
+}
+
 const void* bitmatch_fn(int S, int W, int maxsyms) {
     const int nw = bm_nw(W);
+    if (maxsyms == kBmMaxSymsTiny) return bitmatch_fn_m<kBmMaxSymsTiny>(S, nw);
     return maxsyms == kBmMaxSyms      ? bitmatch_fn_m<kBmMaxSyms>(S, nw)
            : maxsyms == kBmMaxSymsMid ? bitmatch_fn_m<kBmMaxSymsMid>(S, nw)
                                       : bitmatch_fn_m<kBmMaxSymsWide>(S, nw);
@@ -499,10 +519,21 @@ cudaError_t launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, c
     return cudaLaunchKernel(fn, dim3(grid), dim3(a.warps_per_cta * 32), args, smem, st);
 }
 
+void launch_classify(int S, const EncodeArgs& a, uint32_t* lists, uint64_t stride, uint32_t* counts,
+                     int grid, cudaStream_t st) {
+    if (S == 1) plz_classify_kernel<1><<<grid, 128, 0, st>>>(a, lists, stride, counts);
+    else if (S == 2) plz_classify_kernel<2><<<grid, 128, 0, st>>>(a, lists, stride, counts);
+    else plz_classify_kernel<4><<<grid, 128, 0, st>>>(a, lists, stride, counts);
+}
+
 void preload_bitmatch_kernels() {
     for (int S : {1, 2, 4})
         for (int W : {16, 48, 96, 255})
-            for (int m : {kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide}) preload_kernel(bitmatch_fn(S, W, m));
+            for (int m : {kBmMaxSymsTiny, kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide})
+                preload_kernel(bitmatch_fn(S, W, m));
+    preload_kernel(reinterpret_cast<const void*>(plz_classify_kernel<1>));
+    preload_kernel(reinterpret_cast<const void*>(plz_classify_kernel<2>));
+    preload_kernel(reinterpret_cast<const void*>(plz_classify_kernel<4>));
 }
 
 }  // namespace plzgpu

@@ -41,8 +41,10 @@ void fill_assemble_args(plzgpu_ctx* c, const plzgpu_params& p, const Geometry& g
 // the wide-cell pass.  per_sm = 0: the pass does not fit.
 static void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int* wpc_out,
                   int* per_sm_out) {
-    const int pass = maxsyms == 0 ? 0 : (maxsyms == kBmMaxSyms ? 1 : maxsyms == kBmMaxSymsMid ? 5 : 9) +
-                                             __builtin_ctz(unsigned(bm_nw(p.window)));  // 0..12
+    const int pass = maxsyms == 0 ? 0
+                                  : (maxsyms == kBmMaxSyms ? 1 : maxsyms == kBmMaxSymsMid ? 5
+                                                           : maxsyms == kBmMaxSymsWide ? 9 : 13) +
+                                        __builtin_ctz(unsigned(bm_nw(p.window)));  // 0..16
     const int key = pass * 160 + p.symbol_width * 32 + (__builtin_ctz(unsigned(p.chunk_size)) - 10);
     int& wpc = c->enc_wpc[key];
     int& per_sm = c->enc_ctas[key];
@@ -65,6 +67,73 @@ static void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int
     }
     *wpc_out = wpc;
     *per_sm_out = per_sm;
+}
+
+// Latency mode of Kernel I (inputs of at most a few waves of chunks, where a
+// chunk's serial greedy walk — ~0.2 ms at c1 — is the time, not the
+// throughput): every chunk's alphabet is counted first (plz_classify_kernel)
+// and all tiers run at once on their own streams — the 64/32/16-row bitmap
+// passes and the wide-cell pass over their short lists, then the 4-row pass,
+// small enough in shared memory for a whole 16 MiB input in one wave, over
+// the rest — instead of each tier starting when the previous one has found
+// its overflow.  Returns -1 when a tier does not fit (huge chunks): the
+// caller takes the sequential passes.
+static int enqueue_tiers(plzgpu_ctx* c, const plzgpu_params& p, const EncodeArgs& e, uint64_t Gr,
+                         cudaStream_t st, plzgpu_error* err, int* launches) {
+    const int tiers[4] = {kBmMaxSymsTiny, kBmMaxSyms, kBmMaxSymsMid, kBmMaxSymsWide};
+    int wpc[5], per_sm[5];
+    for (int k = 0; k < 4; ++k) {
+        encode_shape(c, p, tiers[k], &wpc[k], &per_sm[k]);
+        if (per_sm[k] == 0) return -1;
+    }
+    encode_shape(c, p, 0, &wpc[4], &per_sm[4]);
+    Meta* m = dmeta(c);
+    CK(c->fb.ensure(6 * Gr * 4 + 16));
+    uint32_t* L = c->fb.as<uint32_t>();  // list k at L + k * Gr; list 5: spills (none expected)
+    CK(cudaMemsetAsync(m->lat_count, 0, sizeof m->lat_count + sizeof m->lat_work, st));
+    launch_classify(p.symbol_width, e, L, Gr, m->lat_count,
+                    int(std::min<uint64_t>(uint64_t(c->sms) * 16, (Gr + 3) / 4)), st);
+    ++*launches;
+    for (int i = 0; i < 4; ++i)
+        if (!c->lat_stream[i]) CK(cudaStreamCreateWithFlags(&c->lat_stream[i], cudaStreamNonBlocking));
+    for (cudaEvent_t& ev : c->lat_ev)
+        if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->lat_ev[0], st));
+    for (int i = 0; i < 4; ++i) CK(cudaStreamWaitEvent(c->lat_stream[i], c->lat_ev[0], 0));
+    auto tier_args = [&](int k) {
+        EncodeArgs b = e;
+        b.work = &m->lat_work[k];
+        b.src_list = L + uint64_t(k) * Gr;
+        b.src_count = &m->lat_count[k];
+        b.classify = 0;
+        for (int i = 0; i < 3; ++i) {
+            b.fb_list[i] = L + 5 * Gr;
+            b.fb_count[i] = &m->lat_count[5];
+        }
+        b.warps_per_cta = wpc[k];
+        return b;
+    };
+    // the short lists first, so their CTAs are placed before the 4-row
+    // pass's fill the SMs (idle CTAs of an empty list exit at once)
+    CK(launch_encode(p.symbol_width, tier_args(4), c->sms * std::max(per_sm[4], 1), c->lat_stream[3]));
+    for (int k = 3; k >= 1; --k)
+        CK(launch_bitmatch(p.symbol_width, tiers[k], tier_args(k), c->sms * per_sm[k],
+                           c->lat_stream[k - 1]));
+    CK(launch_bitmatch(p.symbol_width, tiers[0], tier_args(0), c->sms * per_sm[0], st));
+    *launches += 5;
+    for (int i = 0; i < 4; ++i) {
+        CK(cudaEventRecord(c->lat_ev[1 + i], c->lat_stream[i]));
+        CK(cudaStreamWaitEvent(st, c->lat_ev[1 + i], 0));
+    }
+    // chunks a tier could not hold after all (an exact count makes this list
+    // empty): the wide-cell pass
+    EncodeArgs f = tier_args(4);
+    f.work = &m->lat_work[5];
+    f.src_list = L + 5 * Gr;
+    f.src_count = &m->lat_count[5];
+    CK(launch_encode(p.symbol_width, f, c->sms, st));
+    ++*launches;
+    return PLZGPU_OK;
 }
 
 // Enqueue Kernels I-III for a device-resident input.  img must hold
@@ -138,7 +207,16 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     uint32_t* works[4] = {&m->work[0], &m->work[5], &m->work[9], &m->work[7]};
     int wpc1 = 1, per_sm1 = 0;
     encode_shape(c, p, kBmMaxSyms, &wpc1, &per_sm1);
-    const bool classify = side_passes && Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
+    const bool few = Gr < uint64_t(4) * c->sms * per_sm1 * wpc1;
+    if (few && side_passes && !c->pipe_ready) {
+        const int rc = enqueue_tiers(c, p, e, Gr, st, err, launches);
+        if (rc != -1) {
+            if (rc) return rc;
+            goto scan;
+        }
+    }
+    {
+    const bool classify = side_passes && few;
     e.classify = classify ? 1 : 0;
     cudaError_t launch_err = cudaSuccess;  // first failed bitmap-pass launch
     auto bitmap_pass = [&](int maxsyms, int pass, const uint32_t* src, const uint32_t* src_n,
@@ -213,6 +291,8 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
         ++*launches;
     }
     CK(launch_err);
+    }
+scan:
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
     ScanArgs sa{};

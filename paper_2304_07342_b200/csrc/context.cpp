@@ -58,7 +58,8 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
     DeviceGuard keep;
     cudaSetDevice(c->device);
     for (cudaStream_t sx : {c->stream, c->asm_stream, c->side_stream, c->d2h_stream, c->size_stream,
-                            c->copy_stream})
+                            c->copy_stream, c->lat_stream[0], c->lat_stream[1], c->lat_stream[2],
+                            c->lat_stream[3]})
         if (sx) cudaStreamSynchronize(sx);
     for (DevBuf* b : {&c->in, &c->img, &c->out, &c->pay_slots, &c->flag_slots, &c->psize,
                       &c->fsize, &c->p64, &c->f64, &c->status, &c->agg, &c->incl, &c->desc,
@@ -70,10 +71,12 @@ void plzgpu_ctx_destroy(plzgpu_ctx* c) {
     for (uint8_t* b : c->bounce)
         if (b) cudaFreeHost(b);
     for (cudaStream_t sx : {c->stream, c->asm_stream, c->side_stream, c->d2h_stream, c->size_stream,
-                            c->copy_stream})
+                            c->copy_stream, c->lat_stream[0], c->lat_stream[1], c->lat_stream[2],
+                            c->lat_stream[3]})
         if (sx) cudaStreamDestroy(sx);
     for (cudaEvent_t ev : {c->side_ev[0], c->side_ev[1], c->asm_ev[0], c->asm_ev[1],
-                           c->bounce_ev[0], c->bounce_ev[1], c->bounce_ev[2], c->order_ev})
+                           c->bounce_ev[0], c->bounce_ev[1], c->bounce_ev[2], c->order_ev,
+                           c->lat_ev[0], c->lat_ev[1], c->lat_ev[2], c->lat_ev[3], c->lat_ev[4]})
         if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : c->cont_ev)
         if (ev) cudaEventDestroy(ev);

@@ -169,6 +169,8 @@ struct Meta {
                         // second/third bitmap pass, [7] wide pass
     uint32_t stalled;  // H2D pipeline: a segment never arrived
     uint32_t pad;
+    uint32_t lat_count[8];  // latency mode: chunks per tier list (tiny, 16, 32, 64, wide, spill)
+    uint32_t lat_work[8];   // latency mode: the tier kernels' work counters
     uint64_t range[3];  // plzgpu_decompress_range: output range, total chunks
     ParseResult parse;
 };
@@ -188,8 +190,8 @@ struct plzgpu_ctx {
     int last_launches = 0;
     plzhost::LastOp last_op = plzhost::OP_NONE;
     plzgpu::DecodeArgs last_decode{};
-    int enc_wpc[2240] = {};  // launch shape cache per (pass, S, C)
-    int enc_ctas[2240] = {};
+    int enc_wpc[4096] = {};  // launch shape cache per (pass, S, C)
+    int enc_ctas[4096] = {};
     plzhost::DevBuf fb;          // overflow lists of the bitmap passes (3 x G chunk indices)
     plzhost::DevBuf shard_desc;  // ShardCont / HeaderDesc upload area
     // H2D pipeline of host inputs (plzgpu_compress): segment ready flags
@@ -197,6 +199,8 @@ struct plzgpu_ctx {
     cudaStream_t asm_stream = nullptr;   // pipelined compress: per-container Kernel III
     cudaStream_t side_stream = nullptr;  // Kernel I: the 64-row pass beside the 32-row one
     cudaEvent_t side_ev[2] = {nullptr, nullptr};
+    cudaStream_t lat_stream[4] = {nullptr, nullptr, nullptr, nullptr};  // latency-mode tiers
+    cudaEvent_t lat_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t asm_ev[2] = {nullptr, nullptr};
     // pipelined compress into pinned host memory: per container, its scan
     // and its assembly done; the image goes down on d2h_stream, the

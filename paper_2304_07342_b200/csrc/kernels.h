@@ -60,6 +60,7 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 // mask), so their content is irrelevant — except for row D, the all-zero
 // row standing for position n, which is zeroed over its whole reach (front
 // NW words, bitmap, NW + 3 words behind: the search's one-round look-ahead).
+constexpr int kBmMaxSymsTiny = 4;   // latency mode: chunks with at most 4 symbols
 constexpr int kBmMaxSyms = 16;      // first bitmap pass: all chunks
 constexpr int kBmMaxSymsMid = 32;   // second bitmap pass: the first pass's overflow
 constexpr int kBmMaxSymsWide = 64;  // third bitmap pass: the second pass's overflow
@@ -118,6 +119,13 @@ cudaError_t launch_encode(int S, const EncodeArgs& a, int grid, cudaStream_t st)
 // (maxsyms = kBmMaxSyms, kBmMaxSymsMid or kBmMaxSymsWide)
 cudaError_t launch_bitmatch(int S, int maxsyms, const EncodeArgs& a, int grid, cudaStream_t st);
 int bitmatch_ctas_per_sm(int S, int C, int W, int maxsyms, int warps_per_cta);
+// Latency mode (inputs of a few waves of chunks): every chunk's alphabet is
+// counted first and the chunk listed for the smallest tier that holds it —
+// lists[k * stride + i], k = 0 (<= kBmMaxSymsTiny symbols), 1 (<= kBmMaxSyms),
+// 2 (<= kBmMaxSymsMid), 3 (<= kBmMaxSymsWide), 4 (more: the wide-cell pass),
+// counts[k] — so all tiers can run at once instead of one after the other.
+void launch_classify(int S, const EncodeArgs& a, uint32_t* lists, uint64_t stride, uint32_t* counts,
+                     int grid, cudaStream_t st);
 // full per-position match table (I-aligned searched, else {1,0}); optional raw histogram
 void launch_match_table(int S, const EncodeArgs& a, int grid, uint8_t* len_out, uint8_t* off_out,
                         unsigned long long* raw_hist, cudaStream_t st);
