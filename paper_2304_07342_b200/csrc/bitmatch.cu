@@ -477,16 +477,44 @@ const void* bitmatch_fn_m(int S, int nw) {
     return bitmatch_fn_s<4, MAXS>(nw);
 }
 
-// Latency mode's classification: one warp per chunk (grid-stride).
+// Latency mode's classification: one warp per chunk (grid-stride).  Bytes
+// (S = 1) are counted with a 256-bit presence bitmap in shared memory; wider
+// symbols with count_alphabet.
 template <int S>
 __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_t* lists,
                                                            uint64_t stride, uint32_t* counts) {
+    __shared__ uint32_t seen[4][8];
     const uint32_t lane = lane_id();
+    uint32_t* bm = seen[threadIdx.x >> 5];
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t ck = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
          ck < a.n_chunks; ck += warps) {
         const int n = (ck + 1 == a.n_chunks) ? static_cast<int>(a.last_len) : a.C;
-        const int D = count_alphabet<S>(a.in + ck * uint64_t(a.C) * S, n, lane);
+        int D;
+        if constexpr (S == 1) {
+            if (lane < 8) bm[lane] = 0u;
+            __syncwarp();
+            const uint8_t* src = a.in + ck * uint64_t(a.C);
+            for (int i = 4 * static_cast<int>(lane); i < n; i += 128) {
+                uint32_t v;
+                if (i + 4 <= n && a.bulk_ok) {  // the input base is 16-byte aligned
+                    v = *reinterpret_cast<const uint32_t*>(src + i);
+                } else {
+                    v = src[i];  // past the chunk: repeat its first byte, a no-op for the set
+                    for (int b = 1; b < 4; ++b) v |= uint32_t(i + b < n ? src[i + b] : src[i]) << (8 * b);
+                }
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const uint32_t x = (v >> (8 * b)) & 0xffu;
+                    atomicOr(&bm[x >> 5], 1u << (x & 31u));
+                }
+            }
+            __syncwarp();
+            D = int(__reduce_add_sync(0xffffffffu, lane < 8 ? __popc(bm[lane]) : 0u));
+            __syncwarp();
+        } else {
+            D = count_alphabet<S>(a.in + ck * uint64_t(a.C) * S, n, lane);
+        }
         const int k = D <= kBmMaxSymsTiny ? 0 : D <= kBmMaxSyms ? 1 : D <= kBmMaxSymsMid ? 2
                     : D <= kBmMaxSymsWide ? 3 : 4;
         if (lane == 0) lists[uint64_t(k) * stride + atomicAdd(&counts[k], 1u)] = uint32_t(ck);
