@@ -495,18 +495,20 @@ __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_
             if (lane < 8) bm[lane] = 0u;
             __syncwarp();
             const uint8_t* src = a.in + ck * uint64_t(a.C);
-            for (int i = 4 * static_cast<int>(lane); i < n; i += 128) {
+            for (int base = 0; base < n; base += 128) {  // uniform trip count (match_any)
+                const int i = base + 4 * static_cast<int>(lane);
                 uint32_t v;
                 if (i + 4 <= n && a.bulk_ok) {  // the input base is 16-byte aligned
                     v = *reinterpret_cast<const uint32_t*>(src + i);
-                } else {
-                    v = src[i];  // past the chunk: repeat its first byte, a no-op for the set
-                    for (int b = 1; b < 4; ++b) v |= uint32_t(i + b < n ? src[i + b] : src[i]) << (8 * b);
+                } else {  // past the chunk: repeat its first byte, a no-op for the set
+                    v = 0;
+                    for (int b = 0; b < 4; ++b) v |= uint32_t(i + b < n ? src[i + b] : src[0]) << (8 * b);
                 }
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
+                for (int b = 0; b < 4; ++b) {  // one atomic per distinct value of the warp
                     const uint32_t x = (v >> (8 * b)) & 0xffu;
-                    atomicOr(&bm[x >> 5], 1u << (x & 31u));
+                    const uint32_t same = __match_any_sync(0xffffffffu, x);
+                    if (__ffs(same) - 1 == static_cast<int>(lane)) atomicOr(&bm[x >> 5], 1u << (x & 31u));
                 }
             }
             __syncwarp();

@@ -83,6 +83,7 @@ int plzgpu_shard_encode(plzgpu_ctx* c, const plzgpu_params* params, const void* 
     if (rc) return rc;
     CK(cudaGetLastError());
     c->last_launches = launches;
+    c->last_op = OP_COMPRESS;  // plzgpu_ctx_finish reports the shard's token counts
     // per touched container: local prefix values at its range ends
     c->sh_touch.clear();
     const uint64_t j_first = L ? chunk_begin / g.cpb : 0, j_last = L ? (chunk_end - 1) / g.cpb : 0;

@@ -19,6 +19,7 @@ import subprocess
 import sys
 
 R = sys.argv[1] if len(sys.argv) > 1 else "r1"
+W = sys.argv[2] if len(sys.argv) > 2 else "c5"
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out")
 DST = os.path.join(ROOT, "profiles", R)
@@ -122,7 +123,7 @@ if shares:
     for name, (n, t) in sorted(shares.items(), key=lambda kv: -kv[1][1]):
         lines.append(f"| {name} | {n} | {t / 1e6:.3f} | {100 * t / tot:.1f} % |")
     lines.append("")
-lines += ["## Per-kernel (one `--set full` capture each, c2 workload)", "",
+lines += [f"## Per-kernel (one `--set full` capture each, {W} workload)", "",
           "| kernel | dur µs | DRAM MB (r+w) | DRAM % | SM % | ALU pipe % | FMA pipe % | issue % | occ % | warp-instr |",
           "|---|---|---|---|---|---|---|---|---|---|"]
 for k in kernels:
