@@ -43,7 +43,11 @@ constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSme
 constexpr uint32_t kFastTokens = 2048;
 constexpr uint32_t kFastPtab = kDecodeSmem;
 constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
-constexpr uint32_t kFastWarpSmem = kFastMeta + kDecodeSmem / 4 + 16;
+// the fast path serves S = 2 chunks of at most kDecodeSmem bytes: C <= 2048
+// output positions, 64 waves
+constexpr uint32_t kFastWaves = kDecodeSmem / 2 / 32;
+constexpr uint32_t kFastSrc = kFastMeta + 8 * kFastWaves + 16;  // 32 sources of the wave
+constexpr uint32_t kFastWarpSmem = kFastSrc + 128;
 static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
 constexpr bool kUseFast = true;
 constexpr uint32_t kMainWarpSmem = kUseFast ? kFastWarpSmem : kDecodeWarpSmem;
@@ -424,9 +428,9 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
 //  B. waves of 32 output positions in order: one shared load of the wave's
 //     bitmap + token base, a popcount gives each lane its covering token, one
 //     byte load its offset, and the lane copies out[q - off] (a literal
-//     position copies onto itself).  One shuffle tells whether any source is
-//     an in-wave pointer position (not final yet); only then are the sources
-//     resolved by pointer jumping over the lanes.
+//     position copies onto itself).  A lane whose source is an in-wave
+//     pointer position (not final yet) follows the chain of sources through
+//     the wave's source array in shared memory — no shuffles or votes.
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
@@ -566,20 +570,24 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     // entries, both lookups before the first copy)
     const uint32_t upto = (2u << lane) - 1u;
     uint32_t a_q = s_stage + lane * uint32_t(S);
+    const uint32_t s_src = s_stage + kFastSrc;
     auto wave = [&](uint32_t w, uint32_t off) {
         const int wb = int(w << 5);
         int src = wb + int(lane) - int(off);
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_src + 4u * lane), "r"(src));
+        __syncwarp();
         // a source inside the wave that is a pointer position is not final
-        // yet: resolve by pointer jumping over the lanes' sources (a literal
-        // position is its own source, so a lane whose source lane copies
-        // from elsewhere takes that source; the first step is the check)
-        bool more;
-        do {
-            const bool inw = src >= wb;
-            const int s2 = __shfl_sync(FULL, src, uint32_t(src) & 31u);
-            more = inw && s2 != src;
-            src = inw ? s2 : src;
-        } while (__any_sync(FULL, more));
+        // yet: follow its chain of sources (in the wave's source array) to a
+        // literal position or one before the wave — per lane, no votes; a
+        // literal position is its own source
+        if (off) {
+            while (src >= wb) {
+                int s2;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s2) : "r"(s_src + 4u * uint32_t(src - wb)));
+                if (s2 == src) break;
+                src = s2;
+            }
+        }
         sts_sym<S>(a_q, lds_sym<S>(s_stage + uint32_t(src) * S));
         a_q += 32u * S;
         __syncwarp();
@@ -886,7 +894,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint64_t tok = 0;
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
-    if (kUseFast && !kExact && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
+    if (kUseFast && !kExact && S == 2 && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
     else if (in_smem)

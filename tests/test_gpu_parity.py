@@ -239,6 +239,24 @@ def test_concatenated_images_with_tails():
     assert ref_decompress(joined) == b"".join(parts)
 
 
+def test_concatenated_images_of_mixed_symbol_widths():
+    # one image whose containers alternate S = 2 (the S = 2 decode kernel)
+    # and S = 1 / S = 4 (the other one): both kernels in one call, each
+    # skipping the other's containers; odd output offsets after the tails
+    import torch
+
+    specs = [(2, 255, 2048, 2, 9000), (1, 128, 4096, 1, 7001), (2, 64, 1024, 4, 5003),
+             (4, 255, 1024, 4, 12347), (2, 255, 2048, 1, 2 * 4096 * 3 + 2)]
+    parts = [inputs.make("quant", n, 31 + n, S) for S, _, _, _, n in specs]
+    imgs = [plz.compress(d, P(S, W, Cs, I)) for d, (S, W, Cs, I, _) in zip(parts, specs)]
+    joined = b"".join(imgs)
+    want = b"".join(parts)
+    assert plz.decompress_bytes(joined) == want  # host path
+    d_img = torch.frombuffer(bytearray(joined), dtype=torch.uint8).cuda()
+    assert bytes(plz.decompress_bytes(d_img).cpu().numpy().tobytes()) == want  # resident path
+    assert ref_decompress(joined) == want
+
+
 def test_pinned_host_compress_by_container():
     # A host input of several segments into a pinned host image of several
     # containers takes the per-container pipeline (Kernel III writing into

@@ -21,6 +21,6 @@ for k in plz_scan plz_assemble plz_headers plz_parse; do
 done
 # the decode kernel that takes the S = 2 containers (the other instance only skips)
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:plz_decode_kernel<0, 1>' -s 1 -c 1 \
+    -k regex:plz_decode_kernel -s 3 -c 1 \
     -o gpurun_out/prof_plz_decode_kernel_$R python tools/probe.py $W 1 > /dev/null 2>&1
 ls -la gpurun_out
