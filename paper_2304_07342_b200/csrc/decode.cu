@@ -574,18 +574,21 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     auto wave = [&](uint32_t w, uint32_t off) {
         const int wb = int(w << 5);
         int src = wb + int(lane) - int(off);
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_src + 4u * lane), "r"(src));
-        __syncwarp();
-        // a source inside the wave that is a pointer position is not final
-        // yet: follow its chain of sources (in the wave's source array) to a
-        // literal position or one before the wave — per lane, no votes; a
-        // literal position is its own source
-        if (off) {
-            while (src >= wb) {
-                int s2;
-                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s2) : "r"(s_src + 4u * uint32_t(src - wb)));
-                if (s2 == src) break;
-                src = s2;
+        // off in [1, lane]: the source lies inside the wave (about every other wave).
+        // Only then can it be a pointer position that is not final yet: the
+        // wave's sources go to the source array and each such lane follows
+        // its chain of sources to a literal position or one before the wave
+        // (a literal position is its own source)
+        if (__any_sync(FULL, off - 1u < lane)) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_src + 4u * lane), "r"(src));
+            __syncwarp();
+            if (off) {
+                while (src >= wb) {
+                    int s2;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s2) : "r"(s_src + 4u * uint32_t(src - wb)));
+                    if (s2 == src) break;
+                    src = s2;
+                }
             }
         }
         sts_sym<S>(a_q, lds_sym<S>(s_stage + uint32_t(src) * S));
@@ -979,19 +982,28 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
 // chunk of a container the kernel does not take moves the counter past that
 // container, so the other kernel's containers cost one draw each.
 template <bool kPipe, int kKind>
-__global__ void __launch_bounds__(kDecodeWarps * 32) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
+__global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 8 : 1) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
     const uint32_t lane = lane_id();
     uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kWarpSmem;
     uint32_t* work = a.work + kKind;
     const uint64_t total = a.result->total_chunks;
+    // the container of the warp's last chunk: consecutive draws almost always
+    // fall into it, so the binary search over the descriptors (a chain of
+    // dependent global loads) runs about once per container
+    uint64_t cj = 0, c_lo = 1, c_hi = 0;
     for (;;) {
         uint64_t g = 0;
         if (lane == 0) g = atomicAdd(work, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= total) break;
-        const ContainerDesc d = a.desc[find_container(a.desc, a.result->n_containers, g)];
+        if (g < c_lo || g >= c_hi) {
+            cj = find_container(a.desc, a.result->n_containers, g);
+            c_lo = a.desc[cj].chunk_base;
+            c_hi = c_lo + a.desc[cj].num_chunks;
+        }
+        const ContainerDesc d = a.desc[cj];
         if ((d.S == 2) != (kKind == kKindS2)) {
             if (lane == 0) atomicMax(work, uint32_t(min(total, d.chunk_base + d.num_chunks)));
             continue;
