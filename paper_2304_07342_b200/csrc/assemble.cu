@@ -13,7 +13,11 @@
 //
 // The kernel is a copy at HBM speed, so it is organised around memory
 // round trips:
-//  * one warp per chunk: its two table entries (byte stores by 8 lanes), its
+//  * plz_assemble_tma_kernel (the default when a chunk's slices fit a warp's
+//    8 KiB ring): TMA bulk copies stage up to 8 chunks ahead per warp in
+//    shared memory, the warp writes them out with realigned 128-bit stores;
+//  * plz_assemble_kernel (larger chunks, PLZGPU_ASM_TMA=0): one warp per
+//    chunk, its two table entries (byte stores by 8 lanes), its
 //    flag slice and payload slice (warp_copy2: every source byte of both
 //    loaded before the first store, realigned 128-bit body stores); the next
 //    chunk's prefixes are loaded while this chunk's data is in flight;
@@ -187,8 +191,8 @@ __global__ void __launch_bounds__(128) plz_assemble_kernel(AssembleArgs a) {
             ps_n = a.psize[gn];
             fs_n = a.fsize[gn];
         }
-        const Geo c = locate(a, g);
-        if (c.j != cj) {  // container constants, cached while the warp stays in it
+        if (cj == ~0ull || g - g0 >= n) {  // container constants, cached while the warp stays in it
+            const Geo c = locate(a, g);     // (a 64-bit division)
             cj = c.j;
             g0 = c.g0;
             n = c.n;
@@ -216,6 +220,178 @@ __global__ void __launch_bounds__(128) plz_assemble_kernel(AssembleArgs a) {
         fg = fg_n;
         ps = ps_n;
         fs = fs_n;
+    }
+}
+
+// ------------------------------------------------- TMA-staged Kernel III
+// plz_assemble_tma_kernel: the same image bytes as plz_assemble_kernel, with
+// the loads taken off the registers.  Each warp owns a shared-memory ring
+// (kAsmRing bytes, kAsmSlots mbarriers) and walks its chunks g, g + warps,
+// ...: lane 0 keeps up to kAsmSlots chunks' flag and payload slices in
+// flight as TMA bulk copies (cp.async.bulk, 16-byte rounded, each chunk at
+// the ring's next free 16-byte offset; an allocation that would run past
+// the ring's end starts at 0, and an empty ring restarts at 0), while the warp writes the oldest
+// staged chunk out — byte head to the destination's 16-byte alignment,
+// 128-bit body stores realigned from two aligned shared words, byte tail —
+// and its two table entries.  Per-chunk sizes and prefixes come 32 chunks at
+// a time, one chunk per lane, a batch ahead.  Chunks whose slices exceed the
+// ring (C*S + C/8 + 32 > kAsmRing) take plz_assemble_kernel.
+// 8 KiB rings: ~24 warps/SM (c5: 1.04 ms, DRAM 48 %; 16 KiB rings with 16
+// slots gave 12 warps/SM and 1.32 ms, the register-staged kernel 1.30 ms)
+constexpr int kAsmWarps = 4;
+constexpr uint32_t kAsmRing = 8192;
+constexpr uint32_t kAsmSlots = 8;
+constexpr uint32_t kAsmWarpSmem = kAsmRing + 8 * kAsmSlots;
+
+struct AsmMeta {  // one chunk per lane
+    uint64_t P, F;
+    uint32_t ps, fs;
+};
+
+__device__ __forceinline__ AsmMeta load_meta(const AssembleArgs& a, uint64_t g, uint64_t g_hi) {
+    AsmMeta m{0, 0, 0, 0};
+    if (g < g_hi) {
+        m.P = a.P64[g];
+        m.F = a.F64[g];
+        m.ps = a.psize[g];
+        m.fs = a.fsize[g];
+    }
+    return m;
+}
+
+__device__ __forceinline__ uint32_t r16(uint32_t x) { return (x + 15u) & ~15u; }
+
+__device__ __forceinline__ uint32_t lds_w(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_b(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// Warp copy of len bytes from shared memory (shared-window address src) to
+// dst: byte head to dst's 16-byte alignment, 128-bit body stores each built
+// from five aligned 4-byte shared loads and four funnel shifts, byte tail.
+__device__ __forceinline__ void smem_copy_out(uint8_t* dst, uint32_t src, uint32_t len,
+                                              uint32_t lane) {
+    const uint32_t mis = uint32_t(reinterpret_cast<uintptr_t>(dst) & 15u);
+    const uint32_t head = min((16u - mis) & 15u, len);
+    const uint32_t body = (len - head) >> 4;
+    const uint32_t tail = len - head - 16u * body;
+    if (lane < head) dst[lane] = uint8_t(lds_b(src + lane));
+    uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+    const uint32_t r = 8u * (head & 3u);
+    uint32_t b = src + (head & ~3u) + 16u * lane;
+    for (uint32_t i = lane; i < body; i += 32u, b += 512u) {
+        const uint32_t w0 = lds_w(b), w1 = lds_w(b + 4), w2 = lds_w(b + 8), w3 = lds_w(b + 12),
+                       w4 = lds_w(b + 16);
+        d16[i] = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
+                            __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+    }
+    const uint32_t t0 = head + 16u * body;
+    if (lane < tail) dst[t0 + lane] = uint8_t(lds_b(src + t0 + lane));
+}
+
+__global__ void __launch_bounds__(kAsmWarps * 32) plz_assemble_tma_kernel(AssembleArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    uint8_t* ring = smem + size_t(warp) * kAsmWarpSmem;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(ring + kAsmRing);
+    const uint32_t s_ring = static_cast<uint32_t>(__cvta_generic_to_shared(ring));
+    const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
+    const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
+    const uint64_t g_lo = a.j_lo * a.cpb;
+    const uint64_t g_hi = min(a.n_chunks, j_hi * a.cpb);
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const uint64_t g_first = g_lo + uint64_t(blockIdx.x) * (blockDim.x >> 5) + warp;
+    if (g_first >= g_hi) return;
+    const uint64_t K = (g_hi - g_first + warps - 1) / warps;  // this warp's chunks
+    if (lane < kAsmSlots) mbar_init(&mbar[lane], 1);
+    __syncwarp();
+    // metadata of sequence entries [32b, 32b + 32): cur = the consumer's batch
+    AsmMeta cur = load_meta(a, g_first + warps * lane, g_hi);
+    AsmMeta nxt = load_meta(a, g_first + warps * (32u + lane), g_hi);
+    uint64_t k_issue = 0, k_done = 0;
+    uint32_t wr = 0, rd = 0, infl = 0;
+    uint64_t cj = ~0ull, g0 = 0, n = 0, tabs = 0, pb = 0, fb = 0, ftot = 0;
+    while (k_done < K) {
+        // ---- producer: stage chunks ahead while slots and ring space last
+        while (k_issue < K && k_issue - k_done < kAsmSlots) {
+            const bool in_cur = (k_issue >> 5) == (k_done >> 5);
+            const uint32_t src_lane = uint32_t(k_issue & 31u);
+            const uint32_t ps = __shfl_sync(0xffffffffu, in_cur ? cur.ps : nxt.ps, src_lane);
+            const uint32_t fs = __shfl_sync(0xffffffffu, in_cur ? cur.fs : nxt.fs, src_lane);
+            const uint32_t need = r16(fs) + r16(ps);
+            const bool wrap = wr + need > kAsmRing;  // the rest of the ring is skipped
+            const uint32_t waste = wrap ? kAsmRing - wr : 0u;
+            if (infl + waste + need > kAsmRing) break;
+            const uint32_t at = wrap ? 0u : wr;
+            const uint64_t g = g_first + warps * k_issue;
+            fence_proxy_async_smem();  // this warp's earlier reads of the ring before the TMA writes
+            __syncwarp();
+            if (lane == 0) {
+                uint64_t* mb = &mbar[k_issue % kAsmSlots];
+                const uint32_t m = static_cast<uint32_t>(__cvta_generic_to_shared(mb));
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m),
+                             "r"(need) : "memory");
+                const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(ring + at));
+                if (fs)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                        "l"(a.flag_slots + g * (C / 8)), "r"(r16(fs)), "r"(m) : "memory");
+                if (ps)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d + r16(fs)),
+                        "l"(a.pay_slots + g * C * S), "r"(r16(ps)), "r"(m) : "memory");
+            }
+            wr = at + need;
+            infl += waste + need;
+            ++k_issue;
+        }
+        // ---- consumer: write the oldest staged chunk out
+        const uint32_t src_lane = uint32_t(k_done & 31u);
+        const uint64_t pg = __shfl_sync(0xffffffffu, cur.P, src_lane);
+        const uint64_t fg = __shfl_sync(0xffffffffu, cur.F, src_lane);
+        const uint32_t ps = __shfl_sync(0xffffffffu, cur.ps, src_lane);
+        const uint32_t fs = __shfl_sync(0xffffffffu, cur.fs, src_lane);
+        const uint32_t need = r16(fs) + r16(ps);
+        const bool wrap = rd + need > kAsmRing;  // the producer's allocation, replayed
+        const uint32_t waste = wrap ? kAsmRing - rd : 0u;
+        const uint32_t at = wrap ? 0u : rd;
+        const uint64_t g = g_first + warps * k_done;
+        if (cj == ~0ull || g - g0 >= n) {  // container constants, cached while the warp stays in it
+            const Geo c = locate(a, g);     // (a 64-bit division)
+            cj = c.j;
+            g0 = c.g0;
+            n = c.n;
+            pb = a.P64[g0];
+            fb = a.F64[g0];
+            ftot = a.F64[g0 + n] - fb;
+            tabs = container_start(a, cj, g0) + 26;
+        }
+        const uint64_t pk = pg - pb, fk = fg - fb, k = g - g0;
+        const uint64_t streams = tabs + 8 * (n + 1);
+        if (lane < 4) {
+            a.img[tabs + 4 * k + lane] = uint8_t(pk >> (8 * lane));
+        } else if (lane < 8) {
+            a.img[tabs + 4 * (n + 1) + 4 * k + (lane - 4)] = uint8_t(fk >> (8 * (lane - 4)));
+        }
+        mbar_wait(&mbar[k_done % kAsmSlots], uint32_t(k_done / kAsmSlots) & 1u);
+        smem_copy_out(a.img + streams + fk, s_ring + at, fs, lane);
+        smem_copy_out(a.img + streams + ftot + pk, s_ring + at + r16(fs), ps, lane);
+        __syncwarp();
+        rd = at + need;
+        infl -= waste + need;
+        if (infl == 0) wr = rd = 0;  // ring empty: restart at 0 (so any chunk <= kAsmRing fits)
+        ++k_done;
+        if ((k_done & 31u) == 0u) {  // next batch of metadata
+            cur = nxt;
+            nxt = load_meta(a, g_first + warps * (k_done + 32u + lane), g_hi);
+        }
     }
 }
 
@@ -361,6 +537,25 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     const uint64_t g_lo = a.j_lo * a.cpb;
     const uint64_t g_hi = a.j_hi ? std::min(a.n_chunks, a.j_hi * a.cpb) : a.n_chunks;
     const uint64_t warps_needed = g_hi - g_lo;
+    const uint64_t slices = uint64_t(a.C) * a.S + a.C / 8 + 32;
+    if (assemble_tma_enabled() && slices <= kAsmRing) {
+        static int per_sm = -1;  // same answer on every B200; computed once
+        const size_t smem = size_t(kAsmWarps) * kAsmWarpSmem;
+        if (per_sm < 0) {
+            int blocks = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_assemble_tma_kernel,
+                                                          kAsmWarps * 32, smem);
+            per_sm = blocks > 0 ? blocks : 1;
+        }
+        int sms = 148;
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        uint64_t blocks = (warps_needed + kAsmWarps - 1) / kAsmWarps;
+        blocks = std::min<uint64_t>(blocks, uint64_t(sms) * per_sm);
+        plz_assemble_tma_kernel<<<unsigned(blocks), kAsmWarps * 32, smem, st>>>(a);
+        return;
+    }
     uint64_t blocks = (warps_needed + 3) / 4;
     if (blocks > 148ull * 10) blocks = 148ull * 10;
     plz_assemble_kernel<<<unsigned(blocks), 128, 0, st>>>(a);
@@ -374,6 +569,7 @@ void launch_headers(const AssembleArgs& a, cudaStream_t st) {
 
 void preload_assemble_kernels() {
     preload_kernel(reinterpret_cast<const void*>(plz_assemble_kernel));
+    preload_kernel(reinterpret_cast<const void*>(plz_assemble_tma_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_headers_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_shard_assemble_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_shard_headers_kernel));

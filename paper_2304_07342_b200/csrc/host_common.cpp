@@ -196,6 +196,7 @@ const PipelineConfig& pipeline_config() {
         c.pageable_stage = env_u64("PLZGPU_PAGEABLE_MB", c.pageable_stage, MB, MB);
         c.pageable_min = env_u64("PLZGPU_PAGEABLE_MIN_MB", c.pageable_min, MB, 0);
         c.copy_threads = int(env_u64("PLZGPU_COPY_THREADS", 0, 1, 0));
+        c.asm_tma = env_u64("PLZGPU_ASM_TMA", 1, 1, 0) != 0;
         return c;
     }();
     return cfg;
@@ -240,3 +241,7 @@ uint32_t next_epoch() {
 }
 
 }  // namespace plzhost
+
+namespace plzgpu {
+bool assemble_tma_enabled() { return plzhost::pipeline_config().asm_tma; }
+}  // namespace plzgpu

@@ -172,6 +172,8 @@ struct AssembleArgs {
     uint64_t j_lo, j_hi;
 };
 void launch_assemble(const AssembleArgs& a, cudaStream_t st);
+// Kernel III through the TMA-staged ring (PipelineConfig::asm_tma; host_common.cpp)
+bool assemble_tma_enabled();
 void launch_headers(const AssembleArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------- multi-GPU shards
