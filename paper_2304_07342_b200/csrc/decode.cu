@@ -437,6 +437,16 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     return v;
 }
 
+// Predicated shared-memory stores (no branch around them).
+__device__ __forceinline__ void st_u16_if(bool p, uint32_t a, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}"
+                 ::"r"(a), "r"(v), "r"(uint32_t(p)) : "memory");
+}
+__device__ __forceinline__ void st_u8_if(bool p, uint32_t a, uint32_t v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u8 [%0], %1;\n\t}"
+                 ::"r"(a), "r"(v), "r"(uint32_t(p)) : "memory");
+}
+
 __device__ __forceinline__ uint32_t warp_excl_scan_u32(uint32_t v, uint32_t lane) {
     return warp_incl_scan_u32(v, lane) - v;
 }
@@ -507,6 +517,9 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         bool bad = false;
         uint32_t nreach = 0, o_reach = 0;
         o = 0;
+        // S = 2: tokens 0..navail-1 of the lane have their 2 payload bytes
+        const uint32_t navail = !hf || np <= pin ? 0u : min(8u, (np - pin) >> 1);
+        const uint32_t s_ptl = s_ptab + tbase + 8u * lane;  // the lane's token-table bytes
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t bit = (fb >> (7 - i)) & 1u;
@@ -526,6 +539,22 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                         if (pin + o + uint32_t(b) < np) fld |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
             }
             const bool reached = pos < L;
+            if constexpr (S == 2) {  // branch-free: predicated stores
+                // non-short-circuit forms: no branches around the checks
+                const bool bad_ptr = (len == 0u) | (off == 0u) | (off > pos) | (pos + len > L);
+                const bool b = (uint32_t(i) >= navail) | ((bit != 0u) & bad_ptr);
+                bad |= reached & b;
+                const bool ok = reached & !b;
+                st_u16_if(ok & !bit, s_stage + 2u * pos, fld);
+                // an OR of 0 into the table's first word when the token is not stored
+                atomicOr(ok ? &meta[2u * (pos >> 5)] : meta, ok ? 1u << (pos & 31u) : 0u);
+                st_u8_if(ok, s_ptl + uint32_t(i), off);
+                nreach += ok ? 1u : 0u;
+                o_reach = ok ? o + 2u : o_reach;
+                pos += len;
+                o += 2u;
+                continue;
+            }
             const bool b = !hf || pin + o + sz > np ||
                            (bit && (len == 0u || off == 0u || off > pos || pos + len > L));
             bad |= reached && b;
