@@ -67,6 +67,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
     }
 }
 
+// 1-D TMA bulk copy shared -> global as a bulk group of the issuing thread
+// (SASS: UBLKCP.G.S).  dst/src 16-byte aligned, bytes % 16 == 0.  The
+// writers of src run fence_proxy_async_smem() + a warp barrier first.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(src));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(s),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// Lane 0's bulk stores have read their shared source (the buffer may be
+// rewritten); a no-op without outstanding stores.
+__device__ __forceinline__ void bulk_store_drain(uint32_t lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncwarp();
+}
+// Lane 0's bulk stores are complete (visible in global memory).
+__device__ __forceinline__ void bulk_store_complete(uint32_t lane) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
+}
+
 // Orders this thread's generic-proxy shared-memory accesses before later
 // async-proxy (TMA) writes to the same buffer.
 __device__ __forceinline__ void fence_proxy_async_smem() {

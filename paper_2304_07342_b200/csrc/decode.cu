@@ -595,44 +595,42 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         carry += __shfl_sync(FULL, inc, 31);
     }
     __syncwarp();
-    // ---- phase B: two waves per step (one 16-byte load of both table
-    // entries, both lookups before the first copy)
+    // ---- phase B: waves of 32 positions, two per step (one 16-byte load of
+    // both table entries).  A lane's source q - off is final unless it lies
+    // in the lane's own wave (off <= lane) on a pointer position: then the
+    // lane alone follows the chain through the wave's token lookups (the
+    // covering token of in-wave position s: popcount of the starts up to s)
+    // until it reaches a literal or an earlier wave.  No votes: the chase is
+    // a divergent branch that ~1 wave in 5 takes.
     const uint32_t upto = (2u << lane) - 1u;
     uint32_t a_q = s_stage + lane * uint32_t(S);
-    const uint32_t s_src = s_stage + kFastSrc;
-    auto wave = [&](uint32_t w, uint32_t off) {
-        const int wb = int(w << 5);
-        int src = wb + int(lane) - int(off);
-        // off in [1, lane]: the source lies inside the wave (about every other wave).
-        // Only then can it be a pointer position that is not final yet: the
-        // wave's sources go to the source array and each such lane follows
-        // its chain of sources to a literal position or one before the wave
-        // (a literal position is its own source)
-        if (__any_sync(FULL, off - 1u < lane)) {
-            asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_src + 4u * lane), "r"(src));
-            __syncwarp();
-            if (off) {
-                while (src >= wb) {
-                    int s2;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(s2) : "r"(s_src + 4u * uint32_t(src - wb)));
-                    if (s2 == src) break;
-                    src = s2;
-                }
+    auto wave = [&](uint32_t st, uint32_t tb) {
+        const uint32_t off = lds_u8(tb + __popc(st & upto));
+        int s = int(lane) - int(off);  // in-wave index of the source (< 0: an earlier wave)
+        if (off != 0u && s >= 0) {
+            for (;;) {
+                const uint32_t o2 = lds_u8(tb + __popc(st & ((2u << s) - 1u)));
+                if (o2 == 0u) break;  // a literal: written in phase A
+                s -= int(o2);
+                if (s < 0) break;
             }
         }
-        sts_sym<S>(a_q, lds_sym<S>(s_stage + uint32_t(src) * S));
+        sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (s - int(lane)) * S)));
         a_q += 32u * S;
         __syncwarp();
     };
-    for (uint32_t w = 0; w < nwv; w += 2) {
+    uint32_t w = 0;
+    for (; w + 2u <= nwv; w += 2u) {
         uint32_t st0, tb0, st1, tb1;
         asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                      : "=r"(st0), "=r"(tb0), "=r"(st1), "=r"(tb1) : "r"(s_meta + 8u * w));
-        const uint32_t off0 = lds_u8(tb0 + __popc(st0 & upto));
-        const bool two = w + 1 < nwv;
-        const uint32_t off1 = two ? lds_u8(tb1 + __popc(st1 & upto)) : 0u;
-        wave(w, off0);
-        if (two) wave(w + 1, off1);
+        wave(st0, tb0);
+        wave(st1, tb1);
+    }
+    if (w < nwv) {
+        uint32_t st0, tb0;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(st0), "=r"(tb0) : "r"(s_meta + 8u * w));
+        wave(st0, tb0);
     }
     return true;
 }
@@ -926,6 +924,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint64_t tok = 0;
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
+    bulk_store_drain(lane);  // the previous chunk's stage has left
     if (kUseFast && !kExact && S == 2 && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
@@ -945,7 +944,13 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     if (e == TE_OK && in_smem) {
         __syncwarp();
         const uint64_t bytes = L * S;
-        if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        if (!kPipe && ((reinterpret_cast<uintptr_t>(dst) | bytes) & 15u) == 0) {
+            // one TMA bulk store of the whole stage (the next chunk's
+            // bulk_store_drain waits until it has been read)
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) bulk_s2g(dst, stage, uint32_t(bytes));
+        } else if ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
             uint4* d16 = reinterpret_cast<uint4*>(dst);
             const uint4* s16 = reinterpret_cast<const uint4*>(stage);
             for (uint64_t i = lane; i < (bytes >> 4); i += 32) d16[i] = s16[i];
@@ -1058,6 +1063,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 8 : 1) p
             }
         }
     }
+    bulk_store_complete(lane);
 }
 
 // Chunk-range decode (plzgpu_decompress_range): the output bytes of global
@@ -1099,6 +1105,7 @@ __global__ void plz_chunk_detail_kernel(DecodeArgs a, uint32_t* code, uint64_t* 
     const uint64_t g = *a.err_chunk;
     uint64_t k = 0, tok = 0;
     const uint32_t e = decode_global_chunk<false, true>(a, g, smem, lane_id(), &k, &tok);
+    bulk_store_complete(lane_id());
     if (lane_id() == 0) {
         *code = e;
         *chunk = k;
