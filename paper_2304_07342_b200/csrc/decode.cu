@@ -307,7 +307,7 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
         const uint32_t rel = incl - adv;  // < 32*255
         const uint32_t pos = written + rel;
         const bool reached = pos < L;
-        const bool bad = !has || (bit && (len == 0 || off == 0 || off > pos || pos + len > L));
+        const bool bad = !hf || !has || (bit && (len == 0 || off == 0 || off > pos || pos + len > L));
         const uint32_t m_end = __ballot_sync(0xffffffffu, !reached);
         const uint32_t first_end = m_end ? uint32_t(__ffs(m_end) - 1) : 32u;
         const uint32_t m_err = __ballot_sync(0xffffffffu, bad && reached);
@@ -459,7 +459,6 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);  // pairs {starts, base}
     const uint32_t s_stage = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
     const uint32_t s_ptab = s_stage + kFastPtab;
-    const uint32_t s_meta = s_stage + kFastMeta;
     const uint32_t nwv = (L + 31u) >> 5;
     for (uint32_t w = lane; w < nwv; w += 32) meta[2 * w] = 0u;
     __syncwarp();
@@ -515,10 +514,8 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         uint32_t pos = written + warp_excl_scan_u32(adv, lane);
         // pass 2: checks and writes (tokens from position L on are not read)
         bool bad = false;
-        uint32_t nreach = 0, o_reach = 0;
+        uint32_t nreach = 0, o_reach = 0, lend = 0;
         o = 0;
-        // S = 2: tokens 0..navail-1 of the lane have their 2 payload bytes
-        const uint32_t navail = !hf || np <= pin ? 0u : min(8u, (np - pin) >> 1);
         const uint32_t s_ptl = s_ptab + tbase + 8u * lane;  // the lane's token-table bytes
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -539,20 +536,21 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                         if (pin + o + uint32_t(b) < np) fld |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
             }
             const bool reached = pos < L;
-            if constexpr (S == 2) {  // branch-free: predicated stores
-                // non-short-circuit forms: no branches around the checks
-                const bool bad_ptr = (len == 0u) | (off == 0u) | (off > pos) | (pos + len > L);
-                const bool b = (uint32_t(i) >= navail) | ((bit != 0u) & bad_ptr);
-                bad |= reached & b;
-                const bool ok = reached & !b;
+            if constexpr (S == 2) {
+                // branch-free, predicated stores.  Only the pointer fields are
+                // checked per token; overrun (the last reached token must end
+                // at L), missing payload and missing flags (2T == np, nf ==
+                // ceil(T/8) for T reached tokens) are checked once at the end.
+                // Stores are gated by the flag byte's presence, which bounds
+                // the token table (8 * nf <= kFastTokens).
+                bad |= reached & (bit != 0u) & ((len == 0u) | (off == 0u) | (off > pos));
+                const bool ok = reached & hf;
                 st_u16_if(ok & !bit, s_stage + 2u * pos, fld);
-                // an OR of 0 into the table's first word when the token is not stored
-                atomicOr(ok ? &meta[2u * (pos >> 5)] : meta, ok ? 1u << (pos & 31u) : 0u);
+                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
                 st_u8_if(ok, s_ptl + uint32_t(i), off);
-                nreach += ok ? 1u : 0u;
-                o_reach = ok ? o + 2u : o_reach;
+                nreach += reached ? 1u : 0u;
                 pos += len;
-                o += 2u;
+                lend = reached ? pos : lend;
                 continue;
             }
             const bool b = !hf || pin + o + sz > np ||
@@ -573,12 +571,17 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         const uint32_t end = __shfl_sync(FULL, pos, 31);
         if (end >= L) {  // the walk ends in this step: tokens read, payload consumed
             T = tbase + __reduce_add_sync(FULL, nreach);
-            const uint32_t m = __ballot_sync(FULL, nreach != 0u);
-            in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
+            if constexpr (S == 2) {
+                if (__reduce_max_sync(FULL, lend) != L) return false;  // overrun
+                in_end = 2u * T;
+            } else {
+                const uint32_t m = __ballot_sync(FULL, nreach != 0u);
+                in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
+            }
             break;
         }
         written = end;
-        in = __shfl_sync(FULL, pin + o, 31);
+        in = S == 2 ? in + 512u : __shfl_sync(FULL, pin + o, 31);  // S = 2: 256 two-byte tokens
         tbase += 256u;
     }
     // the walk's end checks (decoder.cpp:58-65)
@@ -591,7 +594,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         const uint32_t w = w0 + lane;
         const uint32_t c = w < nwv ? __popc(meta[2 * w]) : 0u;
         const uint32_t inc = warp_incl_scan_u32(c, lane);
-        if (w < nwv) meta[2 * w + 1] = s_ptab + carry + inc - c - 1u;
+        if (w < nwv) meta[2 * w + 1] = carry + inc - c - 1u;  // token before the wave
         carry += __shfl_sync(FULL, inc, 31);
     }
     __syncwarp();
@@ -604,12 +607,22 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
     // a divergent branch that ~1 wave in 5 takes.
     const uint32_t upto = (2u << lane) - 1u;
     uint32_t a_q = s_stage + lane * uint32_t(S);
-    auto wave = [&](uint32_t st, uint32_t tb) {
-        const uint32_t off = lds_u8(tb + __popc(st & upto));
+    // The token table and the wave table are read-only here: plain loads the
+    // compiler may schedule ahead of the stage copies (each pair's lookups
+    // are issued before the previous pair's copies).
+    const uint4* meta4 = reinterpret_cast<const uint4*>(meta);
+    // (not volatile: the address depends on a wave-table load, which is
+    // ordered after the table writes)
+    auto ptab = [&](uint32_t i) {
+        uint32_t v;
+        asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(s_ptab + i));
+        return v;
+    };
+    auto copy = [&](uint32_t st, uint32_t tb, uint32_t off) {
         int s = int(lane) - int(off);  // in-wave index of the source (< 0: an earlier wave)
         if (off != 0u && s >= 0) {
             for (;;) {
-                const uint32_t o2 = lds_u8(tb + __popc(st & ((2u << s) - 1u)));
+                const uint32_t o2 = ptab(tb + __popc(st & ((2u << s) - 1u)));
                 if (o2 == 0u) break;  // a literal: written in phase A
                 s -= int(o2);
                 if (s < 0) break;
@@ -620,17 +633,26 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         __syncwarp();
     };
     uint32_t w = 0;
-    for (; w + 2u <= nwv; w += 2u) {
-        uint32_t st0, tb0, st1, tb1;
-        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(st0), "=r"(tb0), "=r"(st1), "=r"(tb1) : "r"(s_meta + 8u * w));
-        wave(st0, tb0);
-        wave(st1, tb1);
+    if (nwv >= 2u) {
+        uint4 m = meta4[0];
+        uint32_t off0 = ptab(m.y + __popc(m.x & upto)), off1 = ptab(m.w + __popc(m.z & upto));
+#pragma unroll 2
+        for (; w + 4u <= nwv; w += 2u) {
+            const uint4 mn = meta4[(w >> 1) + 1u];
+            const uint32_t n0 = ptab(mn.y + __popc(mn.x & upto)), n1 = ptab(mn.w + __popc(mn.z & upto));
+            copy(m.x, m.y, off0);
+            copy(m.z, m.w, off1);
+            m = mn;
+            off0 = n0;
+            off1 = n1;
+        }
+        copy(m.x, m.y, off0);
+        copy(m.z, m.w, off1);
+        w += 2u;
     }
     if (w < nwv) {
-        uint32_t st0, tb0;
-        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(st0), "=r"(tb0) : "r"(s_meta + 8u * w));
-        wave(st0, tb0);
+        const uint32_t st = meta[2u * w], tb = meta[2u * w + 1u];
+        copy(st, tb, ptab(tb + __popc(st & upto)));
     }
     return true;
 }
@@ -1026,15 +1048,16 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 8 : 1) p
     // the container of the warp's last chunk: consecutive draws almost always
     // fall into it, so the binary search over the descriptors (a chain of
     // dependent global loads) runs about once per container
-    uint64_t cj = 0, c_lo = 1, c_hi = 0;
+    // (32-bit: the work counter is; fewer live registers across the decode)
+    uint32_t cj = 0, c_lo = 1, c_hi = 0;
     for (;;) {
-        uint64_t g = 0;
+        uint32_t g = 0;
         if (lane == 0) g = atomicAdd(work, 1u);
         g = __shfl_sync(0xffffffffu, g, 0);
         if (g >= total) break;
         if (g < c_lo || g >= c_hi) {
-            cj = find_container(a.desc, a.result->n_containers, g);
-            c_lo = a.desc[cj].chunk_base;
+            cj = uint32_t(find_container(a.desc, a.result->n_containers, g));
+            c_lo = uint32_t(a.desc[cj].chunk_base);
             c_hi = c_lo + a.desc[cj].num_chunks;
         }
         const ContainerDesc d = a.desc[cj];

@@ -382,6 +382,42 @@ def test_corrupted_images_raise_the_reference_error():
     assert same == 300
 
 
+@pytest.mark.parametrize("S,C,kind", [(2, 2048, "quant"), (2, 1024, "runs"), (2, 2048, "alpha"),
+                                       (4, 1024, "quant")])
+def test_corrupted_streams_raise_the_reference_error(S, C, kind):
+    # the fast chunk decoder only accepts or rejects (rejected chunks are
+    # re-walked for the exact error): corruptions of the flag / payload
+    # streams and chunk-boundary shifts (table entries moved within their
+    # neighbours, so the tables stay monotone) must give the reference's
+    # outcome — the same error, or the same bytes
+    import struct
+
+    rng = random.Random(1000 * S + C)
+    data = inputs.make(kind, 3 * C * S + 123 * S, 77, S)
+    img = plz.compress(data, P(S, 255, C, 2))
+    n = struct.unpack_from("<I", img, 21)[0]
+    streams = 26 + 8 * (n + 1)
+    ends = (streams, len(img) - img[25])
+    for it in range(400):
+        bad = bytearray(img)
+        mode = rng.randrange(3)
+        if mode < 2:
+            for _ in range(rng.choice([1, 1, 2, 3])):
+                bad[rng.randrange(*ends)] ^= 1 << rng.randrange(8) if mode else rng.randrange(1, 256)
+        else:
+            table, i = rng.randrange(2), rng.randrange(1, n)
+            at = 26 + table * 4 * (n + 1) + 4 * i
+            lo = struct.unpack_from("<I", bad, at - 4)[0]
+            hi = struct.unpack_from("<I", bad, at + 4)[0]
+            struct.pack_into("<I", bad, at, rng.randint(lo, hi))
+        bad = bytes(bad)
+        mine = _err(plz.decompress_bytes, bad)
+        theirs = _err(ref_decompress, bad)
+        assert mine == theirs, f"iteration {it}"
+        if mine is None:
+            assert plz.decompress_bytes(bad) == ref_decompress(bad)
+
+
 def _table_entry(img, j_container, table, i, value):
     """Overwrite entry i of container j's payload (table 0) or flag (table 1)
     offset table in a concatenated image."""
