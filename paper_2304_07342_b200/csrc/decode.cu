@@ -618,8 +618,11 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(s_ptab + i));
         return v;
     };
-    auto copy = [&](uint32_t st, uint32_t tb, uint32_t off) {
-        int s = int(lane) - int(off);  // in-wave index of the source (< 0: an earlier wave)
+    // Source of the lane's position in a wave: in-wave index (< 0: an
+    // earlier wave, final).  Reads only the token and wave tables, so the
+    // next pair's sources are resolved before this pair's copies.
+    auto source = [&](uint32_t st, uint32_t tb, uint32_t off) {
+        int s = int(lane) - int(off);
         if (off != 0u && s >= 0) {
             for (;;) {
                 const uint32_t o2 = ptab(tb + __popc(st & ((2u << s) - 1u)));
@@ -628,31 +631,44 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                 if (s < 0) break;
             }
         }
+        return s;
+    };
+    auto sources = [&](const uint4& m, int& s0, int& s1) {
+        const uint32_t off0 = ptab(m.y + __popc(m.x & upto)), off1 = ptab(m.w + __popc(m.z & upto));
+        s0 = int(lane) - int(off0);
+        s1 = int(lane) - int(off1);
+        // one divergent region per pair, entered by ~1 pair in 3
+        // (off - 1 < lane, unsigned: 0 < off <= lane — a source in the wave)
+        if ((off0 - 1u < lane) | (off1 - 1u < lane)) {
+            s0 = source(m.x, m.y, off0);
+            s1 = source(m.z, m.w, off1);
+        }
+    };
+    auto copy = [&](int s) {
         sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (s - int(lane)) * S)));
         a_q += 32u * S;
         __syncwarp();
     };
     uint32_t w = 0;
     if (nwv >= 2u) {
-        uint4 m = meta4[0];
-        uint32_t off0 = ptab(m.y + __popc(m.x & upto)), off1 = ptab(m.w + __popc(m.z & upto));
+        int s0, s1;
+        sources(meta4[0], s0, s1);
 #pragma unroll 2
         for (; w + 4u <= nwv; w += 2u) {
-            const uint4 mn = meta4[(w >> 1) + 1u];
-            const uint32_t n0 = ptab(mn.y + __popc(mn.x & upto)), n1 = ptab(mn.w + __popc(mn.z & upto));
-            copy(m.x, m.y, off0);
-            copy(m.z, m.w, off1);
-            m = mn;
-            off0 = n0;
-            off1 = n1;
+            int n0, n1;
+            sources(meta4[(w >> 1) + 1u], n0, n1);
+            copy(s0);
+            copy(s1);
+            s0 = n0;
+            s1 = n1;
         }
-        copy(m.x, m.y, off0);
-        copy(m.z, m.w, off1);
+        copy(s0);
+        copy(s1);
         w += 2u;
     }
     if (w < nwv) {
         const uint32_t st = meta[2u * w], tb = meta[2u * w + 1u];
-        copy(st, tb, ptab(tb + __popc(st & upto)));
+        copy(source(st, tb, ptab(tb + __popc(st & upto))));
     }
     return true;
 }
