@@ -259,7 +259,7 @@ __device__ __forceinline__ AsmMeta load_meta(const AssembleArgs& a, uint64_t g, 
     return m;
 }
 
-__device__ __forceinline__ uint32_t r16(uint32_t x) { return (x + 15u) & ~15u; }
+__host__ __device__ __forceinline__ uint32_t r16(uint32_t x) { return (x + 15u) & ~15u; }
 
 __device__ __forceinline__ uint32_t lds_w(uint32_t a) {
     uint32_t v;
@@ -392,6 +392,179 @@ __global__ void __launch_bounds__(kAsmWarps * 32) plz_assemble_tma_kernel(Assemb
             cur = nxt;
             nxt = load_meta(a, g_first + warps * (k_done + 32u + lane), g_hi);
         }
+    }
+}
+
+// ------------------------------------------------- batched Kernel III
+// plz_assemble_batch_kernel: the same image bytes, with the per-chunk
+// bookkeeping done once per run of 32 consecutive chunks, one chunk per
+// lane: each lane finds its chunk's container (header geometry, stream
+// offsets), writes its two table entries and computes both destinations; a
+// warp scan of the staged sizes cuts the run into batches (chunk c joins
+// batch floor(excl_c / kAbSplit), so a batch spans at most kAbSplit plus one
+// chunk's slices) and each batch is staged by one TMA bulk copy per slice,
+// issued by the chunk's own lane on the buffer's mbarrier.  Two buffers per
+// warp: batch b + 1 is in flight while batch b is written out chunk by chunk
+// (byte head + tail in one predicated pass, realigned 128-bit body stores).
+// The next run's metadata is loaded while this run is written.
+constexpr int kAbWarps = 4;
+constexpr uint32_t kAbSplit = 4096;
+constexpr uint32_t kAbBuf = 8704;  // kAbSplit + the largest slices it serves (C*S <= 4 KiB: + C/8 <= 512 B)
+constexpr uint32_t kAbWarpSmem = 2 * kAbBuf + 16;
+constexpr uint64_t kAbMinChunks = 1ull << 17;  // below: the TMA ring kernel
+
+struct AbChunk {  // one chunk per lane
+    uint64_t P, F;
+    uint32_t ps, fs;
+};
+
+__device__ __forceinline__ AbChunk ab_load(const AssembleArgs& a, uint64_t g, uint64_t g_hi) {
+    AbChunk m{0, 0, 0, 0};
+    if (g < g_hi) {
+        m.P = a.P64[g];
+        m.F = a.F64[g];
+        m.ps = a.psize[g];
+        m.fs = a.fsize[g];
+    }
+    return m;
+}
+
+// Warp copy of one staged slice: byte head to dst's 16-byte alignment and
+// byte tail in one predicated pass (lanes 0-15 head, 16-31 tail), then the
+// body as realigned 128-bit stores (five aligned shared loads, four funnel
+// shifts per word).
+__device__ __forceinline__ void ab_copy(uint8_t* dst, uint32_t src, uint32_t len, uint32_t lane) {
+    const uint32_t head = min((16u - uint32_t(reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u, len);
+    const uint32_t body = (len - head) >> 4;
+    const uint32_t tail = len - head - 16u * body;
+    const uint32_t jb = lane & 15u;
+    const uint32_t o = lane < 16u ? jb : head + 16u * body + jb;
+    if (jb < (lane < 16u ? head : tail)) dst[o] = uint8_t(lds_b(src + o));
+    uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+    const uint32_t r = 8u * (head & 3u);
+    uint32_t b = src + (head & ~3u) + 16u * lane;
+    for (uint32_t i = lane; i < body; i += 32u, b += 512u) {
+        const uint32_t w0 = lds_w(b), w1 = lds_w(b + 4), w2 = lds_w(b + 8), w3 = lds_w(b + 12),
+                       w4 = lds_w(b + 16);
+        d16[i] = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
+                            __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+    }
+}
+
+__global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(AssembleArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t lane = lane_id();
+    const uint32_t warp = threadIdx.x >> 5;
+    uint8_t* wbase = smem + size_t(warp) * kAbWarpSmem;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + 2 * kAbBuf);
+    const uint32_t s_buf = static_cast<uint32_t>(__cvta_generic_to_shared(wbase));
+    const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
+    const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
+    const uint64_t g_lo = a.j_lo * a.cpb;
+    const uint64_t g_hi = min(a.n_chunks, j_hi * a.cpb);
+    const uint64_t n_runs = (g_hi - g_lo + 31) / 32;
+    const uint64_t warps = uint64_t(gridDim.x) * kAbWarps;
+    uint64_t r = uint64_t(blockIdx.x) * kAbWarps + warp;
+    if (r >= n_runs) return;
+    if (lane < 2) mbar_init(&mbar[lane], 1);
+    __syncwarp();
+    uint32_t phase = 0;  // bit i: parity of buffer i's next completion
+    uint32_t issued = 0; // batches issued so far (buffer = issued & 1)
+    AbChunk cur = ab_load(a, g_lo + 32 * r + lane, g_hi);
+    for (; r < n_runs; r += warps) {
+        const uint64_t g = g_lo + 32 * r + lane;
+        const bool live = g < g_hi;
+        AbChunk nxt = ab_load(a, g_lo + 32 * (r + warps) + lane, g_hi);
+        // ---- per-lane geometry: container, table entries, destinations
+        uint8_t* dst_f = a.img;
+        uint8_t* dst_p = a.img;
+        if (live) {
+            const uint64_t j = g / a.cpb;
+            const uint64_t g0 = j * a.cpb;
+            const uint64_t n = (j + 1 == a.n_blocks) ? a.n_chunks - g0 : a.cpb;
+            const uint64_t pb = a.P64[g0], fb = a.F64[g0];
+            const uint64_t ftot = a.F64[g0 + n] - fb;
+            const uint64_t tabs = 26u * j + 8u * (g0 + j) + pb + fb + 26u;
+            const uint64_t k = g - g0;
+            const uint32_t pk = uint32_t(cur.P - pb), fk = uint32_t(cur.F - fb);
+            uint8_t* tp = a.img + tabs + 4 * k;
+            uint8_t* tf = a.img + tabs + 4 * (n + 1) + 4 * k;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                tp[b] = uint8_t(pk >> (8 * b));
+                tf[b] = uint8_t(fk >> (8 * b));
+            }
+            const uint64_t streams = tabs + 8 * (n + 1);
+            dst_f = a.img + streams + (cur.F - fb);
+            dst_p = a.img + streams + ftot + (cur.P - pb);
+        }
+        // ---- batches: exclusive scan of the staged sizes
+        const uint32_t z = live ? r16(cur.fs) + r16(cur.ps) : 0u;
+        uint32_t incl = z;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= uint32_t(d)) incl += x;
+        }
+        const uint32_t excl = incl - z;
+        // batch of chunk c: floor(excl_c / kAbSplit); batch values only grow
+        // with c but may skip one (a chunk larger than kAbSplit)
+        const uint32_t bat = live ? excl / kAbSplit : 0xffffffffu;
+        auto issue = [&](uint32_t bv) {  // returns the buffer
+            const uint32_t m = __ballot_sync(0xffffffffu, bat == bv);
+            const uint32_t c0 = __ffs(m) - 1, c1 = 31 - __clz(m);
+            const uint32_t base = __shfl_sync(0xffffffffu, excl, c0);
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, c1) - base;
+            const uint32_t buf = issued & 1u;
+            const uint32_t s_mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[buf]));
+            fence_proxy_async_smem();  // earlier reads of this buffer before the TMA writes
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_mb),
+                             "r"(total) : "memory");
+            __syncwarp();
+            if (bat == bv) {
+                const uint32_t d = s_buf + buf * kAbBuf + (excl - base);
+                if (cur.fs)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                        "l"(a.flag_slots + g * (C / 8)), "r"(r16(cur.fs)), "r"(s_mb) : "memory");
+                if (cur.ps)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d + r16(cur.fs)),
+                        "l"(a.pay_slots + g * C * S), "r"(r16(cur.ps)), "r"(s_mb) : "memory");
+            }
+            ++issued;
+            return buf;
+        };
+        uint32_t bv = __shfl_sync(0xffffffffu, bat, 0);  // lane 0 is always live
+        uint32_t buf = issue(bv);
+        for (;;) {
+            const uint32_t bn = __reduce_min_sync(0xffffffffu, bat > bv ? bat : 0xffffffffu);
+            const uint32_t buf_n = bn != 0xffffffffu ? issue(bn) : 0u;
+            mbar_wait(&mbar[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
+            uint32_t m = __ballot_sync(0xffffffffu, bat == bv);
+            const uint32_t base = __shfl_sync(0xffffffffu, excl, __ffs(m) - 1);
+            while (m) {
+                const uint32_t c = __ffs(m) - 1;
+                m &= m - 1;
+                uint8_t* df = reinterpret_cast<uint8_t*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst_f), c));
+                uint8_t* dp = reinterpret_cast<uint8_t*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst_p), c));
+                const uint32_t fs = __shfl_sync(0xffffffffu, cur.fs, c);
+                const uint32_t ps = __shfl_sync(0xffffffffu, cur.ps, c);
+                const uint32_t src = s_buf + buf * kAbBuf + __shfl_sync(0xffffffffu, excl, c) - base;
+                ab_copy(df, src, fs, lane);
+                ab_copy(dp, src + r16(fs), ps, lane);
+            }
+            __syncwarp();
+            if (bn == 0xffffffffu) break;
+            bv = bn;
+            buf = buf_n;
+        }
+        cur = nxt;
     }
 }
 
@@ -538,7 +711,30 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     const uint64_t g_hi = a.j_hi ? std::min(a.n_chunks, a.j_hi * a.cpb) : a.n_chunks;
     const uint64_t warps_needed = g_hi - g_lo;
     const uint64_t slices = uint64_t(a.C) * a.S + a.C / 8 + 32;
-    if (assemble_tma_enabled() && slices <= kAsmRing) {
+    const int mode = assemble_mode();
+    // batched runs need enough of them to fill the GPU (c5: 65k runs; c1's
+    // 128 runs took 23 us against the ring's 8 us)
+    if (mode >= 2 && warps_needed >= kAbMinChunks &&
+        r16(uint32_t(a.C) * a.S) + r16(uint32_t(a.C) / 8) <= kAbBuf - kAbSplit) {
+        static int per_sm = -1;  // same answer on every B200; computed once
+        const size_t smem = size_t(kAbWarps) * kAbWarpSmem;
+        if (per_sm < 0) {
+            int blocks = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_assemble_batch_kernel,
+                                                          kAbWarps * 32, smem);
+            per_sm = blocks > 0 ? blocks : 1;
+        }
+        int sms = 148;
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess)
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const uint64_t runs = (warps_needed + 31) / 32;
+        uint64_t blocks = (runs + kAbWarps - 1) / kAbWarps;
+        blocks = std::min<uint64_t>(blocks, uint64_t(sms) * per_sm);
+        plz_assemble_batch_kernel<<<unsigned(blocks), kAbWarps * 32, smem, st>>>(a);
+        return;
+    }
+    if (mode >= 1 && slices <= kAsmRing) {
         static int per_sm = -1;  // same answer on every B200; computed once
         const size_t smem = size_t(kAsmWarps) * kAsmWarpSmem;
         if (per_sm < 0) {
@@ -570,6 +766,7 @@ void launch_headers(const AssembleArgs& a, cudaStream_t st) {
 void preload_assemble_kernels() {
     preload_kernel(reinterpret_cast<const void*>(plz_assemble_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_assemble_tma_kernel));
+    preload_kernel(reinterpret_cast<const void*>(plz_assemble_batch_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_headers_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_shard_assemble_kernel));
     preload_kernel(reinterpret_cast<const void*>(plz_shard_headers_kernel));

@@ -196,7 +196,7 @@ const PipelineConfig& pipeline_config() {
         c.pageable_stage = env_u64("PLZGPU_PAGEABLE_MB", c.pageable_stage, MB, MB);
         c.pageable_min = env_u64("PLZGPU_PAGEABLE_MIN_MB", c.pageable_min, MB, 0);
         c.copy_threads = int(env_u64("PLZGPU_COPY_THREADS", 0, 1, 0));
-        c.asm_tma = env_u64("PLZGPU_ASM_TMA", 1, 1, 0) != 0;
+        c.asm_mode = int(env_u64("PLZGPU_ASM_MODE", 2, 1, 0));
         return c;
     }();
     return cfg;
@@ -243,5 +243,5 @@ uint32_t next_epoch() {
 }  // namespace plzhost
 
 namespace plzgpu {
-bool assemble_tma_enabled() { return plzhost::pipeline_config().asm_tma; }
+int assemble_mode() { return plzhost::pipeline_config().asm_mode; }
 }  // namespace plzgpu

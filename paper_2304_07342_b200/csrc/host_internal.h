@@ -86,7 +86,7 @@ struct PipelineConfig {
     uint64_t pageable_stage = 64u << 20;  // PLZGPU_PAGEABLE_MB: one pinned bounce slot
     uint64_t pageable_min = 64u << 20;    // PLZGPU_PAGEABLE_MIN_MB: staged copies from this size on
     int copy_threads = 0;                 // PLZGPU_COPY_THREADS: host copy workers (0: cores - 1, <= 15)
-    bool asm_tma = true;                  // PLZGPU_ASM_TMA=0: Kernel III with register-staged loads
+    int asm_mode = 2;                     // PLZGPU_ASM_MODE: Kernel III 0 register-staged, 1 TMA ring, 2 batched runs
 };
 const PipelineConfig& pipeline_config();
 

@@ -172,8 +172,9 @@ struct AssembleArgs {
     uint64_t j_lo, j_hi;
 };
 void launch_assemble(const AssembleArgs& a, cudaStream_t st);
-// Kernel III through the TMA-staged ring (PipelineConfig::asm_tma; host_common.cpp)
-bool assemble_tma_enabled();
+// Kernel III variant (PipelineConfig::asm_mode; host_common.cpp): 0 register-staged,
+// 1 TMA ring, 2 batched runs (default)
+int assemble_mode();
 void launch_headers(const AssembleArgs& a, cudaStream_t st);
 
 // ---------------------------------------------------- multi-GPU shards
