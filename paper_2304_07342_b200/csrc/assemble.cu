@@ -408,9 +408,10 @@ __global__ void __launch_bounds__(kAsmWarps * 32) plz_assemble_tma_kernel(Assemb
 // (byte head + tail in one predicated pass, realigned 128-bit body stores).
 // The next run's metadata is loaded while this run is written.
 constexpr int kAbWarps = 4;
-constexpr uint32_t kAbSplit = 4096;
-constexpr uint32_t kAbBuf = 8704;  // kAbSplit + the largest slices it serves (C*S <= 4 KiB: + C/8 <= 512 B)
-constexpr uint32_t kAbWarpSmem = 2 * kAbBuf + 16;
+constexpr uint32_t kAbSplit = 2048;
+constexpr uint32_t kAbMaxSlices = 4608;  // C*S <= 4 KiB: + C/8 <= 512 B
+// a buffer holds kAbSplit + one chunk's largest slices (sized per launch)
+__host__ __device__ __forceinline__ uint32_t ab_warp_smem(uint32_t buf) { return 2 * buf + 16; }
 constexpr uint64_t kAbMinChunks = 1ull << 17;  // below: the TMA ring kernel
 
 struct AbChunk {  // one chunk per lane
@@ -451,12 +452,12 @@ __device__ __forceinline__ void ab_copy(uint8_t* dst, uint32_t src, uint32_t len
     }
 }
 
-__global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(AssembleArgs a) {
+__global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(AssembleArgs a, uint32_t buf_bytes) {
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
-    uint8_t* wbase = smem + size_t(warp) * kAbWarpSmem;
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + 2 * kAbBuf);
+    uint8_t* wbase = smem + size_t(warp) * ab_warp_smem(buf_bytes);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + 2 * buf_bytes);
     const uint32_t s_buf = static_cast<uint32_t>(__cvta_generic_to_shared(wbase));
     const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
     const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
                              "r"(total) : "memory");
             __syncwarp();
             if (bat == bv) {
-                const uint32_t d = s_buf + buf * kAbBuf + (excl - base);
+                const uint32_t d = s_buf + buf * buf_bytes + (excl - base);
                 if (cur.fs)
                     asm volatile(
                         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
                     __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst_p), c));
                 const uint32_t fs = __shfl_sync(0xffffffffu, cur.fs, c);
                 const uint32_t ps = __shfl_sync(0xffffffffu, cur.ps, c);
-                const uint32_t src = s_buf + buf * kAbBuf + __shfl_sync(0xffffffffu, excl, c) - base;
+                const uint32_t src = s_buf + buf * buf_bytes + __shfl_sync(0xffffffffu, excl, c) - base;
                 ab_copy(df, src, fs, lane);
                 ab_copy(dp, src + r16(fs), ps, lane);
             }
@@ -714,16 +715,14 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     const int mode = assemble_mode();
     // batched runs need enough of them to fill the GPU (c5: 65k runs; c1's
     // 128 runs took 23 us against the ring's 8 us)
-    if (mode >= 2 && warps_needed >= kAbMinChunks &&
-        r16(uint32_t(a.C) * a.S) + r16(uint32_t(a.C) / 8) <= kAbBuf - kAbSplit) {
-        static int per_sm = -1;  // same answer on every B200; computed once
-        const size_t smem = size_t(kAbWarps) * kAbWarpSmem;
-        if (per_sm < 0) {
-            int blocks = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, plz_assemble_batch_kernel,
-                                                          kAbWarps * 32, smem);
-            per_sm = blocks > 0 ? blocks : 1;
-        }
+    const uint32_t ab_slices = r16(uint32_t(a.C) * a.S) + r16(uint32_t(a.C) / 8);
+    if (mode >= 2 && warps_needed >= kAbMinChunks && ab_slices <= kAbMaxSlices) {
+        const uint32_t buf = kAbSplit + ab_slices;
+        const size_t smem = size_t(kAbWarps) * ab_warp_smem(buf);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, plz_assemble_batch_kernel,
+                                                      kAbWarps * 32, smem);
+        if (per_sm < 1) per_sm = 1;
         int sms = 148;
         int dev = 0;
         if (cudaGetDevice(&dev) == cudaSuccess)
@@ -731,7 +730,7 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
         const uint64_t runs = (warps_needed + 31) / 32;
         uint64_t blocks = (runs + kAbWarps - 1) / kAbWarps;
         blocks = std::min<uint64_t>(blocks, uint64_t(sms) * per_sm);
-        plz_assemble_batch_kernel<<<unsigned(blocks), kAbWarps * 32, smem, st>>>(a);
+        plz_assemble_batch_kernel<<<unsigned(blocks), kAbWarps * 32, smem, st>>>(a, buf);
         return;
     }
     if (mode >= 1 && slices <= kAsmRing) {
