@@ -286,6 +286,15 @@ int plzgpu_pointer_histogram(plzgpu_ctx* ctx, const plzgpu_params* params, const
 int plzgpu_profile_encode(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
                           uint64_t n, void* stream, plzgpu_error* err);
 
+/* Per-stage CUDA-event times of a device-resident compress (bench.py's
+ * per-kernel rooflines): ms[0] Kernel I (match + encode), ms[1] Kernel II
+ * (global scan), ms[2] Kernel III + headers (deflate / container assembly),
+ * each the mean over `steps` compresses of `d_in` into `d_img` (capacity
+ * `cap` >= plzgpu_compress_bound).  The image is complete after the call. */
+int plzgpu_profile_stages(plzgpu_ctx* ctx, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* d_img, uint64_t cap, int steps, double* ms,
+                          void* stream, plzgpu_error* err);
+
 /* Measured int32 lane-op throughput of `device` (lane operations per
  * second): op 0 = LOP3, 1 = IADD, 2 = SHF (funnel shift), 3 = POPC + IADD.
  * The denominator of the matching kernel's integer roofline (SURVEY.md

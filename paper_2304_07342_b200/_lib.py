@@ -80,6 +80,8 @@ SIGNATURES = [  # every entry point of include/plzgpu.h
     ("plzgpu_ctx_finish", C.c_int, [_VP, _VP, C.POINTER(Stats), _E]),
     ("plzgpu_decompress_chunk", C.c_int, [_VP, _VP, _U64, _VP, _U64, _U64, _P, _U64, _VP, _E]),
     ("plzgpu_profile_encode", C.c_int, [_VP, _P, _VP, _U64, _VP, _E]),
+    ("plzgpu_profile_stages", C.c_int, [_VP, _P, _VP, _U64, _VP, _U64, C.c_int,
+                                        C.POINTER(C.c_double), _VP, _E]),
     ("plzgpu_int_peak", C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double), _E]),
     ("plzgpu_match_table", C.c_int, [_VP, _P, _VP, _U64, _VP, _VP, C.POINTER(_U64), _VP, _E]),
     ("plzgpu_pointer_histogram", C.c_int, [_VP, _P, _VP, _U64, C.POINTER(_U64), _VP, _E]),

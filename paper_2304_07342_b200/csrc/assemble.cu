@@ -441,14 +441,16 @@ __device__ __forceinline__ void ab_copy(uint8_t* dst, uint32_t src, uint32_t len
     const uint32_t jb = lane & 15u;
     const uint32_t o = lane < 16u ? jb : head + 16u * body + jb;
     if (jb < (lane < 16u ? head : tail)) dst[o] = uint8_t(lds_b(src + o));
+    // body word i = source bytes [head + 16 i, +16): two aligned 16-byte
+    // shared loads, the five words from (head >> 2) on (uniform per slice),
+    // funnel-shifted by head & 3 bytes
     uint4* d16 = reinterpret_cast<uint4*>(dst + head);
-    const uint32_t r = 8u * (head & 3u);
-    uint32_t b = src + (head & ~3u) + 16u * lane;
+    uint32_t b = src + 16u * lane;
     for (uint32_t i = lane; i < body; i += 32u, b += 512u) {
-        const uint32_t w0 = lds_w(b), w1 = lds_w(b + 4), w2 = lds_w(b + 8), w3 = lds_w(b + 12),
-                       w4 = lds_w(b + 16);
-        d16[i] = make_uint4(__funnelshift_r(w0, w1, r), __funnelshift_r(w1, w2, r),
-                            __funnelshift_r(w2, w3, r), __funnelshift_r(w3, w4, r));
+        uint4 x, y;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x.x), "=r"(x.y), "=r"(x.z), "=r"(x.w) : "r"(b));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(y.x), "=r"(y.y), "=r"(y.z), "=r"(y.w) : "r"(b + 16));
+        d16[i] = realign(x, y, head);
     }
 }
 

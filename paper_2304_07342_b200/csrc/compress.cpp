@@ -143,6 +143,27 @@ static int enqueue_tiers(plzgpu_ctx* c, const plzgpu_params& p, const EncodeArgs
 // slots and exclusive prefixes P64/F64[0..G] in the context.
 // g0/g1 (a pipelined compress, one container at a time): only chunks
 // [g0, g1) of the G; their prefixes continue from P64/F64[g0].
+// Kernel II over chunks [g0, g0 + Gr) of the context's size arrays (status
+// words and the tile counter cleared by the Kernel I enqueue).
+static void enqueue_scan(plzgpu_ctx* c, uint64_t g0, uint64_t Gr, cudaStream_t st) {
+    Meta* m = dmeta(c);
+    ScanArgs sa{};
+    sa.psize = c->psize.as<uint32_t>() + g0;
+    sa.fsize = c->fsize.as<uint32_t>() + g0;
+    sa.n = Gr;
+    sa.P64 = c->p64.as<uint64_t>() + g0;
+    sa.F64 = c->f64.as<uint64_t>() + g0;
+    if (g0) {  // continue the earlier containers' totals
+        sa.carry_p = c->p64.as<uint64_t>() + g0;
+        sa.carry_f = c->f64.as<uint64_t>() + g0;
+    }
+    sa.status = c->status.as<uint32_t>();
+    sa.agg = c->agg.as<ulonglong2>();
+    sa.incl = c->incl.as<ulonglong2>();
+    sa.tile_counter = &m->work[1];
+    launch_scan(sa, st);
+}
+
 int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_in, uint64_t G,
                         uint32_t last_len, cudaStream_t st, plzgpu_error* err, int* launches,
                         bool scan, uint64_t g0, uint64_t g1, bool side_passes) {
@@ -295,21 +316,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
 scan:
     if (!scan) return PLZGPU_OK;
     // ---- Kernel II
-    ScanArgs sa{};
-    sa.psize = e.psize;
-    sa.fsize = e.fsize;
-    sa.n = Gr;
-    sa.P64 = c->p64.as<uint64_t>() + g0;
-    sa.F64 = c->f64.as<uint64_t>() + g0;
-    if (g0) {  // continue the earlier containers' totals
-        sa.carry_p = c->p64.as<uint64_t>() + g0;
-        sa.carry_f = c->f64.as<uint64_t>() + g0;
-    }
-    sa.status = c->status.as<uint32_t>();
-    sa.agg = c->agg.as<ulonglong2>();
-    sa.incl = c->incl.as<ulonglong2>();
-    sa.tile_counter = &m->work[1];
-    launch_scan(sa, st);
+    enqueue_scan(c, g0, Gr, st);
     ++*launches;
     return PLZGPU_OK;
 }
@@ -442,6 +449,52 @@ int plzgpu_profile_encode(plzgpu_ctx* c, const plzgpu_params* params, const void
     CK(cudaSetDevice(c->device));
     return enqueue_compress(c, *params, static_cast<const uint8_t*>(d_in), n, nullptr, nullptr,
                             pick(c, stream), err, 1);
+}
+
+
+int plzgpu_profile_stages(plzgpu_ctx* c, const plzgpu_params* params, const void* d_in,
+                          uint64_t n, void* d_img, uint64_t cap, int steps, double* ms,
+                          void* stream, plzgpu_error* err) {
+    clear_err(err);
+    int rc = validate_fields(*params, err);
+    if (rc) return rc;
+    ms[0] = ms[1] = ms[2] = 0.0;
+    if (n == 0 || steps <= 0) return PLZGPU_OK;
+    if (cap < plzgpu_compress_bound(n, params))
+        return set_err(err, PLZGPU_CAPACITY, 0, kNoIndex, kNoIndex, "image buffer below compress_bound");
+    DeviceGuard keep;
+    CK(cudaSetDevice(c->device));
+    const cudaStream_t st = pick(c, stream);
+    const plzgpu_params& p = *params;
+    const Geometry g = geometry(n, p);
+    cudaEvent_t ev[4];
+    for (cudaEvent_t& e : ev) CK(cudaEventCreate(&e));
+    int launches = 0;
+    for (int s = 0; s < steps && rc == PLZGPU_OK; ++s) {
+        CK(cudaEventRecord(ev[0], st));
+        rc = enqueue_encode_scan(c, p, static_cast<const uint8_t*>(d_in), g.n_chunks, g.last_len,
+                                 st, err, &launches, false);
+        if (rc) break;
+        CK(cudaEventRecord(ev[1], st));
+        if (g.n_chunks) enqueue_scan(c, 0, g.n_chunks, st);
+        CK(cudaEventRecord(ev[2], st));
+        AssembleArgs a{};
+        fill_assemble_args(c, p, g, static_cast<const uint8_t*>(d_in), static_cast<uint8_t*>(d_img),
+                           &dmeta(c)->img_len, &a);
+        if (g.n_chunks) launch_assemble(a, st);
+        launch_headers(a, st);
+        CK(cudaEventRecord(ev[3], st));
+        CK(cudaEventSynchronize(ev[3]));
+        for (int k = 0; k < 3; ++k) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, ev[k], ev[k + 1]));
+            ms[k] += t / steps;
+        }
+    }
+    for (cudaEvent_t& e : ev) cudaEventDestroy(e);
+    CK(cudaGetLastError());
+    c->last_op = OP_NONE;
+    return rc;
 }
 
 }  // extern "C"

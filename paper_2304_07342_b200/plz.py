@@ -263,6 +263,16 @@ class Context:
         _check(L.lib().plzgpu_profile_encode(self.handle, C.byref(params.to_c()), C.c_void_p(d_in),
                                              n, C.c_void_p(stream or None), C.byref(e)), e)
 
+    def profile_stages(self, params: Params, d_in: int, n: int, d_img: int, cap: int,
+                       steps: int = 3, stream: int = 0):
+        """CUDA-event ms of Kernel I, Kernel II and Kernel III + headers
+        (plzgpu_profile_stages), each the mean over `steps` compresses."""
+        ms, e = (C.c_double * 3)(), L.Error()
+        _check(L.lib().plzgpu_profile_stages(self.handle, C.byref(params.to_c()), C.c_void_p(d_in),
+                                             n, C.c_void_p(d_img), cap, steps, ms,
+                                             C.c_void_p(stream or None), C.byref(e)), e)
+        return tuple(ms)
+
     def finish(self, stream: int = 0):
         st, e = L.Stats(), L.Error()
         _check(L.lib().plzgpu_ctx_finish(self.handle, C.c_void_p(stream or None), C.byref(st),
