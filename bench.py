@@ -389,6 +389,10 @@ def run_b200(args):
     # ---- Kernel I alone (the roofline numerator) on this rank's bytes
     enc_ms = reduce(encode_kernel_ms(ctx, params, d_in, n, stream, args.steps),
                     dist.ReduceOp.MAX if world > 1 else None)
+    # ---- per-stage CUDA-event times (Kernels I, II, III + headers) of the
+    # same compress, for the scan and deflate rooflines (north_star)
+    stage_ms = (ctx.profile_stages(params, d_in.data_ptr(), n, img.data_ptr(), img.numel(),
+                                   max(3, min(args.steps, 5)), sh) if world == 1 else None)
 
     # ---- decompress (device-resident)
     if world == 1:
@@ -557,6 +561,7 @@ def run_b200(args):
             "frac": dec_gbs / peak, "peak_kind": peak_kind, "bytes_per_step": dec_bytes,
             "traffic": dprof["dram_bytes"] if dprof else None,
             "source": dprof["source"] if dprof else None},
+        "stages": stage_rooflines(stage_ms, n_chunks, img_len, peak, peak_kind),
         "tokens": {"pointer": ptr_tok, "literal": lit_tok},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
@@ -576,6 +581,31 @@ def run_b200(args):
         dist.destroy_process_group()
     print(json.dumps(line), flush=True)
     return 0
+
+
+def stage_rooflines(stage_ms, n_chunks, img_len, peak, peak_kind):
+    """HBM rooflines of Kernel II (global scan: psize/fsize read, P64/F64
+    written — 24 B per chunk) and Kernel III + headers (staged slices read,
+    image written, 24 B of prefixes/sizes per chunk read) from the live
+    per-stage CUDA-event times (plzgpu_profile_stages), with the ncu DRAM
+    traffic of the committed capture beside each."""
+    if not stage_ms:
+        return None
+    out = {"source": "plzgpu_profile_stages (CUDA events on the launch stream, mean of the steps)",
+           "kernel_I_ms": stage_ms[0]}
+    for key, ms, name, nbytes, pat in (
+            ("kernel_II", stage_ms[1], "plz_scan_kernel (decoupled look-back scan)",
+             24 * n_chunks, "plz_scan_kernel"),
+            ("kernel_III", stage_ms[2], "plz_assemble_batch_kernel + plz_headers_kernel (deflate)",
+             2 * img_len + 24 * n_chunks, "plz_assemble")):
+        prof = ncu_profile_facts(pat)
+        gbs = nbytes / (ms * 1e-3) / 1e9 if ms > 0 else None
+        out[key] = {"kernel": name, "ms": ms, "bound": "hbm", "bytes": nbytes, "achieved": gbs,
+                    "peak": peak, "unit": "GB/s", "frac": gbs / peak if gbs else None,
+                    "peak_kind": peak_kind,
+                    "traffic": prof["dram_bytes"] if prof else None,
+                    "source": prof["source"] if prof else None}
+    return out
 
 
 def pageable_e2e(ctx, params, d_in, n, img_len, stream, sh, timed, steps):
