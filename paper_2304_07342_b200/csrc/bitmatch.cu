@@ -495,6 +495,26 @@ __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_
             if (lane < 8) bm[lane] = 0u;
             __syncwarp();
             const uint8_t* src = a.in + ck * uint64_t(a.C);
+            if (n == a.C && n <= 4096 && a.bulk_ok) {
+                // whole chunk of at most 4 KiB, 16-byte aligned: every lane's
+                // 16-byte words loaded up front (one memory round trip per
+                // chunk instead of one per 128 bytes)
+                uint4 v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (512 * k < n) v[k] = *reinterpret_cast<const uint4*>(src + 512 * k + 16 * lane);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    if (512 * k >= n) break;
+                    const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+                    for (int b = 0; b < 16; ++b) {  // one atomic per distinct value of the warp
+                        const uint32_t x = (w4[b >> 2] >> (8 * (b & 3))) & 0xffu;
+                        const uint32_t same = __match_any_sync(0xffffffffu, x);
+                        if (__ffs(same) - 1 == static_cast<int>(lane)) atomicOr(&bm[x >> 5], 1u << (x & 31u));
+                    }
+                }
+            } else
             for (int base = 0; base < n; base += 128) {  // uniform trip count (match_any)
                 const int i = base + 4 * static_cast<int>(lane);
                 uint32_t v;
