@@ -85,3 +85,22 @@ def test_c5_fields_sharded_equal_single_gpu():
         got = dist.simulate_sharded(p, data, world)
         assert torch.equal(got, want), f"sharded image differs at {world} ranks"
     assert torch.equal(plz.decompress_bytes(want), data)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("S,kind", [(1, "quant"), (2, "quant")])
+def test_batched_assembly_across_odd_containers(S, kind):
+    # Kernel III's batched runs (inputs of >= 128 Ki chunks) over containers
+    # of 1021 chunks — runs of 32 straddle container boundaries — and a
+    # partial last chunk plus (S = 2) a tail byte, against the reference image
+    import inputs
+
+    C = 1024
+    n = (131072 + 77) * C * S + 700 * S + (S - 1)
+    data = inputs.make(kind, n, 5, S)
+    p = plz.validate(plz.Params(S, 64, C, 1, 1021 * C * S))
+    img = plz.compress(data, p)
+    op = O.make_params(S, 64, C, 1, 1021 * C * S)
+    ref = O.ref_compress(data, op, 0)
+    assert img == ref, "image differs from the reference"
+    assert plz.decompress_bytes(img) == data
