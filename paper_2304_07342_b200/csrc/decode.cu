@@ -40,14 +40,15 @@ constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSme
 // that takes decode_chunk_smem), wave table (per 32 output positions:
 // token-start bitmap + address of the token before the wave; read two
 // entries at a time, so one spare entry).
-constexpr uint32_t kFastTokens = 2048;
+constexpr uint32_t kFastTokens = 1024;  // c5 chunks carry at most ~600 tokens; a chunk with more
+                                        // (over half literals) takes decode_chunk_smem.  1024 and
+                                        // 9 CTAs/SM measured +2.9 % on c5 against 2048 and 8
 constexpr uint32_t kFastPtab = kDecodeSmem;
 constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
 // the fast path serves S = 2 chunks of at most kDecodeSmem bytes: C <= 2048
 // output positions, 64 waves
 constexpr uint32_t kFastWaves = kDecodeSmem / 2 / 32;
-constexpr uint32_t kFastSrc = kFastMeta + 8 * kFastWaves + 16;  // 32 sources of the wave
-constexpr uint32_t kFastWarpSmem = kFastSrc + 128;
+constexpr uint32_t kFastWarpSmem = kFastMeta + 8 * kFastWaves + 16;  // + the spare table pair
 static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
 constexpr bool kUseFast = true;
 constexpr uint32_t kMainWarpSmem = kUseFast ? kFastWarpSmem : kDecodeWarpSmem;
@@ -1054,7 +1055,7 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
 // chunk of a container the kernel does not take moves the counter past that
 // container, so the other kernel's containers cost one draw each.
 template <bool kPipe, int kKind>
-__global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 8 : 1) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
+__global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 9 : 1) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
     const uint32_t lane = lane_id();
