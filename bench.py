@@ -507,7 +507,7 @@ def run_b200(args):
         if _lib.lib().plzgpu_int_peak(local, op, ctypes.byref(v), ctypes.byref(e)) == 0:
             int_peaks[name] = v.value
     nw = [1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]
-    prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {nw}, 16>")
+    prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {nw}, 12>")
     dprof = ncu_profile_facts("plz_decode_kernel")
     pairs = match_pairs(n, w)
     pairs_s = pairs / (enc_ms * 1e-3)
@@ -535,7 +535,7 @@ def run_b200(args):
                        "ms_per_step": d_ms, "roundtrip_ok": roundtrip_ok},
         "e2e": e2e,
         "roofline": {
-            "kernel": f"plz_bitmatch_kernel<{w.S},{nw},16> (Kernel I: match + greedy walk + encode)",
+            "kernel": f"plz_bitmatch_kernel<{w.S},{nw},12> (Kernel I: match + greedy walk + encode)",
             "bound": "int32-alu",
             "achieved": pairs_s / 1e9,
             "peak": lane_peak / 1e9 if lane_peak else None,

@@ -29,8 +29,8 @@
 //
 // Occurrence bitmaps need one row per distinct symbol of the chunk (quant
 // codes: 3-9 per 2048-symbol chunk).  The chunk's symbols are renamed to
-// ids 0..D-1 (first occurrence order).  The first pass keeps 16 rows per
-// warp (28 warps/SM at c2); a chunk with more distinct symbols is listed for
+// ids 0..D-1 (first occurrence order).  The first pass keeps 12 rows per
+// warp (36 warps/SM at c5, register-bound; 16 rows fitted 30: 2.5 % slower); a chunk with more distinct symbols is listed for
 // a second bitmap pass with 32 rows, then a third with 64, and one with more
 // than 64 for the wide-cell pass (encode.cu), which handles any alphabet.
 #include "common.cuh"
@@ -169,8 +169,8 @@ __device__ __forceinline__ bool rename_symbols(uint8_t* raw, int n, uint2* tbl, 
                                                int& D, uint32_t (&tab)[(MAXS + 31) / 32]) {
     using T = typename Sym<S>::T;
     constexpr uint32_t kEmpty = 0xffffffffu;
-    constexpr int H = 2 * MAXS;  // table slots: load factor <= 1/2
-    constexpr int HB = MAXS == 4 ? 3 : MAXS == 16 ? 5 : MAXS == 32 ? 6 : 7;
+    constexpr int H = bm_hash_slots(MAXS);  // table slots: load factor <= 1/2
+    constexpr int HB = H == 8 ? 3 : H == 16 ? 4 : H == 32 ? 5 : H == 64 ? 6 : 7;
     static_assert((1 << HB) == H, "hash size");
 #pragma unroll
     for (int i = 0; i < (H + 31) / 32; ++i)
@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(kBmMaxThreads) plz_bitmatch_kernel(EncodeArgs 
     uint8_t* base = smem + bm_warp_smem(C, S, W, MAXS) * warp;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base);
     uint2* tbl = reinterpret_cast<uint2*>(base + 16);
-    uint8_t* raw = base + 16 + 2 * MAXS * 8;
+    uint8_t* raw = base + 16 + bm_hash_slots(MAXS) * 8;
     uint8_t* ids = raw;
     uint32_t* rows = reinterpret_cast<uint32_t*>(raw + C + kBmIdPad);
 

@@ -72,7 +72,7 @@ static void encode_shape(plzgpu_ctx* c, const plzgpu_params& p, int maxsyms, int
 // Latency mode of Kernel I (inputs of at most a few waves of chunks, where a
 // chunk's serial greedy walk — ~0.2 ms at c1 — is the time, not the
 // throughput): every chunk's alphabet is counted first (plz_classify_kernel)
-// and all tiers run at once on their own streams — the 64/32/16-row bitmap
+// and all tiers run at once on their own streams — the 64/32/12-row bitmap
 // passes and the wide-cell pass over their short lists, then the 4-row pass,
 // small enough in shared memory for a whole 16 MiB input in one wave, over
 // the rest — instead of each tier starting when the previous one has found
@@ -215,7 +215,7 @@ int enqueue_encode_scan(plzgpu_ctx* c, const plzgpu_params& p, const uint8_t* d_
     e.seg_chunks = c->pipe_seg_chunks;
     e.stalled = &m->stalled;
     e.hist = c->enc_hist;
-    // bitmap pass (16 rows) over every chunk, then the 32-row and 64-row
+    // bitmap pass (12 rows) over every chunk, then the 32-row and 64-row
     // passes over what overflowed, then the wide-cell pass.  With few chunks
     // per resident warp the later passes' tails would add up, so the first
     // pass then sorts its overflow by exact alphabet size and the 32- and

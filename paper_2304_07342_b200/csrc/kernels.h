@@ -61,7 +61,7 @@ __host__ __device__ inline size_t encode_warp_smem(int C, int S) {
 // row standing for position n, which is zeroed over its whole reach (front
 // NW words, bitmap, NW + 3 words behind: the search's one-round look-ahead).
 constexpr int kBmMaxSymsTiny = 4;   // latency mode: chunks with at most 4 symbols
-constexpr int kBmMaxSyms = 16;      // first bitmap pass: all chunks
+constexpr int kBmMaxSyms = 12;      // first bitmap pass: all chunks (12 rows: 36 warps/SM at c5)
 constexpr int kBmMaxSymsMid = 32;   // second bitmap pass: the first pass's overflow
 constexpr int kBmMaxSymsWide = 64;  // third bitmap pass: the second pass's overflow
 constexpr int kBmMaxThreads = 128;   // CTA size bound (registers: up to 255 per thread)
@@ -76,8 +76,12 @@ __host__ __device__ inline size_t bm_region(int C, int S, int W, int maxsyms) {
     const size_t rows = size_t(C) + kBmIdPad + size_t(bm_rows_words(C, W, maxsyms)) * 4;
     return (raw > rows ? raw : rows) + 16;
 }
+// renaming hash table: a power of two >= 2 * maxsyms slots (load factor <= 1/2)
+__host__ __device__ constexpr int bm_hash_slots(int maxsyms) {
+    return maxsyms <= 4 ? 8 : maxsyms <= 8 ? 16 : maxsyms <= 16 ? 32 : maxsyms <= 32 ? 64 : 128;
+}
 __host__ __device__ inline size_t bm_warp_smem(int C, int S, int W, int maxsyms) {
-    const size_t b = 16 + size_t(2 * maxsyms) * 8 + bm_region(C, S, W, maxsyms);
+    const size_t b = 16 + size_t(bm_hash_slots(maxsyms)) * 8 + bm_region(C, S, W, maxsyms);
     return (b + 15) & ~size_t(15);
 }
 

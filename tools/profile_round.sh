@@ -11,9 +11,9 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 # every launch of one compress + decompress step (serialised, cold): shares, not absolutes
 PLZGPU_NO_PIPE=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:plz_ --csv \
     --log-file gpurun_out/launches_$R.csv python tools/probe.py $W 1 > /dev/null 2>&1
-# Kernel I: the first bitmap pass (16 rows) of the second compress call
+# Kernel I: the first bitmap pass (12 rows) of the second compress call
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:plz_bitmatch_kernel<.*16>' -s 1 -c 1 \
+    -k 'regex:plz_bitmatch_kernel<.*12>' -s 1 -c 1 \
     -o gpurun_out/prof_plz_bitmatch_$R python tools/probe.py $W 1 > /dev/null 2>&1
 for k in plz_scan plz_assemble plz_headers plz_parse; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
