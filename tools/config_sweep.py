@@ -11,7 +11,7 @@ c5  u16 8 GiB (32 NYX-like fields), W=255, I=2, one GPU
 One JSON line per (config, I): compress / decompress GB/s of input bytes
 (device-resident, CUDA events, warm-up first, inputs > L2 except c1), ratio,
 round-trip check.  --cpu adds the reference library on all host threads over
-the first 16 MiB of each config (bench.py --impl reference), for the ratio /
+the stream's first container of each config (bench.py --impl reference), for the ratio /
 throughput beside it.
 """
 import argparse
@@ -78,16 +78,17 @@ def run(ctx, d_in, params, steps):
 
 
 def cpu_ref(name, I):
-    """The reference library on all host cores over the first 16 MiB, through
-    bench.py's reference arm (the one place outside tests/ that runs oracle/)."""
+    """The reference library on all host cores over the stream's first
+    container (256 MiB, or the whole input when smaller), through bench.py's
+    reference arm (the one place outside tests/ that runs oracle/)."""
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                        "--workload", name, "--interval", str(I), "--steps", "2", "--warmup", "0",
-                        "--cpu-sample-mib", "16"], capture_output=True, text=True)
+                        "--workload", name, "--interval", str(I), "--steps", "2", "--warmup", "0"],
+                       capture_output=True, text=True)
     try:
         d = json.loads(r.stdout.strip().splitlines()[-1])
-        return {"cpu_compress_gbs": d["value"], "cpu_ratio": d["ratio"],
-                "cpu_cores": d["cpu_baseline"]["cores"],
-                "cpu_sample_bytes": d["config"]["bytes_per_step"]}
+        return {"cpu_compress_gbs": d["value"], "cpu_decompress_gbs": d["decompress"]["value"],
+                "cpu_ratio": d["ratio"], "cpu_cores": d["cpu_baseline"]["cores"],
+                "cpu_sample_bytes": d["cpu_baseline"]["sample_bytes"]}
     except (IndexError, KeyError, ValueError):
         return None
 
