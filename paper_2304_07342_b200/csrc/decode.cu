@@ -421,11 +421,15 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
 // runs in two lean phases:
 //
 //  A. tokens, 256 per step: lane l owns flag byte l of the step and walks its
-//     8 tokens itself (their payload fields are contiguous: S = 2 reads its 16
-//     bytes as 5 aligned words, other widths byte by byte), so one warp scan
-//     per 256 tokens places them.  Literals go straight to the stage, every
-//     token start is set in its wave's start bitmap and its offset (0 for a
-//     literal) lands in the token table.
+//     8 tokens itself (S = 2: their 16 payload bytes as 5 aligned words; the
+//     8 lengths and offsets as two byte-permuted words each, literals masked
+//     to length 1 / offset 0 by the flag byte spread to a byte mask, the
+//     length sum by two 4-byte dot products), so one warp scan per 256 tokens
+//     places them.  The 8 offsets land in the token table as one 8-byte
+//     store; per token, the literal goes to the stage and the token start
+//     into its wave's start bitmap.  Steps before the last need no
+//     reached-token bookkeeping (zero pointer fields by a zero-byte test of
+//     the packed words).
 //  B. waves of 32 output positions in order: one shared load of the wave's
 //     bitmap + token base, a popcount gives each lane its covering token, one
 //     byte load its offset, and the lane copies out[q - off] (a literal
@@ -469,37 +473,101 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         const uint32_t fidx = fb0 + lane;
         const bool hf = fidx < nf;
         const uint32_t fb = hf ? uint32_t(flags[fidx]) : 0u;
-        uint32_t pin, wv[4] = {0u, 0u, 0u, 0u};
         if constexpr (S == 2) {
-            pin = in + 16u * lane;  // every token is 2 payload bytes
-            const uintptr_t a = reinterpret_cast<uintptr_t>(pay) + pin;
-            const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-            const uintptr_t lim = reinterpret_cast<uintptr_t>(pay) + np;
-            uint32_t x[5];
+            // The lane's 8 tokens are its 16 payload bytes (every token is 2
+            // bytes): 5 aligned words, funnel-shifted; token 2k is the low
+            // half of wv[k], [len][off].  Lengths and offsets of 4 tokens per
+            // word (byte permutes), pointer tokens as a byte mask from the
+            // flag byte, the step's length sum by two 4-byte dot products.
+            uint32_t wv[4];
+            {
+                const uintptr_t a = reinterpret_cast<uintptr_t>(pay) + in + 16u * lane;
+                const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+                const uintptr_t lim = reinterpret_cast<uintptr_t>(pay) + np;
+                uint32_t x[5];
 #pragma unroll
-            for (int k = 0; k < 5; ++k)
-                x[k] = reinterpret_cast<uintptr_t>(wp + k) < lim ? wp[k] : 0u;
-            const uint32_t sh = 8u * uint32_t(a & 3u);
+                for (int k = 0; k < 5; ++k)
+                    x[k] = reinterpret_cast<uintptr_t>(wp + k) < lim ? wp[k] : 0u;
+                const uint32_t sh = 8u * uint32_t(a & 3u);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) wv[k] = __funnelshift_r(x[k], x[k + 1], sh);
-        } else {
-            const uint32_t p = __popc(fb);
-            pin = in + warp_excl_scan_u32(2u * p + uint32_t(S) * (8u - p), lane);
+                for (int k = 0; k < 4; ++k) wv[k] = __funnelshift_r(x[k], x[k + 1], sh);
+            }
+            const uint32_t r = __brev(fb) >> 24;  // bit i: token i is a pointer (MSB-first flags)
+            const uint32_t pm0 = (((r & 15u) * 0x204081u) & 0x01010101u) * 255u;
+            const uint32_t pm1 = ((((r >> 4) & 15u) * 0x204081u) & 0x01010101u) * 255u;
+            // lengths (a literal: 1) and offsets (a literal: 0), tokens 0-3 / 4-7
+            const uint32_t lm0 = (__byte_perm(wv[0], wv[1], 0x6420) & pm0) | (~pm0 & 0x01010101u);
+            const uint32_t lm1 = (__byte_perm(wv[2], wv[3], 0x6420) & pm1) | (~pm1 & 0x01010101u);
+            const uint32_t om0 = __byte_perm(wv[0], wv[1], 0x7531) & pm0;
+            const uint32_t om1 = __byte_perm(wv[2], wv[3], 0x7531) & pm1;
+            const uint32_t adv = __dp4a(lm0, 0x01010101u, 0u) + __dp4a(lm1, 0x01010101u, 0u);
+            uint32_t pos = written + warp_excl_scan_u32(adv, lane);
+            const uint32_t end = __shfl_sync(FULL, pos + adv, 31);
+            // token table: the 8 offsets at once (tokens past the flag bytes
+            // are never stored: that bounds the table, 8 * nf <= kFastTokens)
+            if (hf)
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(s_ptab + tbase + 8u * lane),
+                             "r"(om0), "r"(om1) : "memory");
+            bool bad = false;
+            if (end < L) {
+                // every token of the step is reached: zero pointer fields by a
+                // zero-byte test of the packed words, per token only the
+                // offset-before-start check, the literal store and the start bit
+                auto zero_byte = [](uint32_t v) { return ((v - 0x01010101u) & ~v & 0x80808080u) != 0u; };
+                bad = zero_byte(lm0) | zero_byte(lm1) | zero_byte(om0 | ~pm0) | zero_byte(om1 | ~pm1);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const uint32_t len = ((i < 4 ? lm0 : lm1) >> (8 * (i & 3))) & 0xffu;
+                    const uint32_t off = ((i < 4 ? om0 : om1) >> (8 * (i & 3))) & 0xffu;
+                    const uint32_t fld = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
+                    bad |= off > pos;
+                    st_u16_if(((r >> i) & 1u) == 0u, s_stage + 2u * pos, fld);
+                    atomicOr(&meta[2u * (pos >> 5)], 1u << (pos & 31u));
+                    pos += len;
+                }
+                if (__any_sync(FULL, bad)) return false;
+                written = end;
+                in += 512u;  // 256 two-byte tokens
+                tbase += 256u;
+                continue;
+            }
+            // the walk ends in this step: tokens from position L on are not
+            // read.  Per token only the pointer fields; overrun (the last
+            // reached token must end at L), missing payload and missing flag
+            // bits (2T == np, nf == ceil(T/8) for T reached tokens) once.
+            uint32_t nreach = 0, lend = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t len = ((i < 4 ? lm0 : lm1) >> (8 * (i & 3))) & 0xffu;
+                const uint32_t off = ((i < 4 ? om0 : om1) >> (8 * (i & 3))) & 0xffu;
+                const uint32_t fld = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
+                const uint32_t bit = (r >> i) & 1u;
+                const bool reached = pos < L;
+                bad |= reached & ((len == 0u) | ((bit != 0u) & (off == 0u)) | (off > pos));
+                const bool ok = reached & hf;
+                st_u16_if(ok & !bit, s_stage + 2u * pos, fld);
+                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
+                nreach += reached ? 1u : 0u;
+                pos += len;
+                lend = reached ? pos : lend;
+            }
+            if (__any_sync(FULL, bad)) return false;
+            T = tbase + __reduce_add_sync(FULL, nreach);
+            if (__reduce_max_sync(FULL, lend) != L) return false;  // overrun
+            in_end = 2u * T;
+            break;
         }
-        // pass 1: token fields and lengths (S = 2 re-derives them from the
-        // four payload words in pass 2 instead of keeping 24 registers)
-        uint32_t lpk[2] = {0u, 0u}, opk[2] = {0u, 0u};  // other widths: lengths / offsets, 4 per word
+        // other widths (not dispatched here; kept generic): payload offsets
+        // by a warp scan, fields byte by byte
+        const uint32_t pin = in + warp_excl_scan_u32(2u * __popc(fb) + uint32_t(S) * (8u - __popc(fb)), lane);
+        // pass 1: token fields and lengths
+        uint32_t lpk[2] = {0u, 0u}, opk[2] = {0u, 0u};  // lengths / offsets, 4 per word
         uint32_t adv = 0, o = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t bit = (fb >> (7 - i)) & 1u;
-            uint32_t f;
-            if constexpr (S == 2) {
-                f = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
-                adv += bit ? (f & 0xffu) : 1u;
-                continue;
-            } else {
-                f = 0;
+            uint32_t f = 0;
+            {
                 const uint32_t sz = bit ? 2u : uint32_t(S);
 #pragma unroll
                 for (int b = 0; b < (S > 2 ? S : 2); ++b)
@@ -515,45 +583,20 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         uint32_t pos = written + warp_excl_scan_u32(adv, lane);
         // pass 2: checks and writes (tokens from position L on are not read)
         bool bad = false;
-        uint32_t nreach = 0, o_reach = 0, lend = 0;
+        uint32_t nreach = 0, o_reach = 0;
         o = 0;
-        const uint32_t s_ptl = s_ptab + tbase + 8u * lane;  // the lane's token-table bytes
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t bit = (fb >> (7 - i)) & 1u;
             const uint32_t sz = bit ? 2u : uint32_t(S);
-            uint32_t len, off, fld;
-            if constexpr (S == 2) {
-                fld = (i & 1) ? (wv[i >> 1] >> 16) : (wv[i >> 1] & 0xffffu);
-                len = bit ? (fld & 0xffu) : 1u;
-                off = bit ? (fld >> 8) : 0u;
-            } else {
-                len = (lpk[i >> 2] >> (8 * (i & 3))) & 0xffu;
-                off = (opk[i >> 2] >> (8 * (i & 3))) & 0xffu;
-                fld = 0;
-                if (!bit)  // a literal's S bytes, read again
+            const uint32_t len = (lpk[i >> 2] >> (8 * (i & 3))) & 0xffu;
+            const uint32_t off = (opk[i >> 2] >> (8 * (i & 3))) & 0xffu;
+            uint32_t fld = 0;
+            if (!bit)  // a literal's S bytes, read again
 #pragma unroll
-                    for (int b = 0; b < S; ++b)
-                        if (pin + o + uint32_t(b) < np) fld |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
-            }
+                for (int b = 0; b < S; ++b)
+                    if (pin + o + uint32_t(b) < np) fld |= uint32_t(pay[pin + o + uint32_t(b)]) << (8 * b);
             const bool reached = pos < L;
-            if constexpr (S == 2) {
-                // branch-free, predicated stores.  Only the pointer fields are
-                // checked per token; overrun (the last reached token must end
-                // at L), missing payload and missing flags (2T == np, nf ==
-                // ceil(T/8) for T reached tokens) are checked once at the end.
-                // Stores are gated by the flag byte's presence, which bounds
-                // the token table (8 * nf <= kFastTokens).
-                bad |= reached & (bit != 0u) & ((len == 0u) | (off == 0u) | (off > pos));
-                const bool ok = reached & hf;
-                st_u16_if(ok & !bit, s_stage + 2u * pos, fld);
-                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
-                st_u8_if(ok, s_ptl + uint32_t(i), off);
-                nreach += reached ? 1u : 0u;
-                pos += len;
-                lend = reached ? pos : lend;
-                continue;
-            }
             const bool b = !hf || pin + o + sz > np ||
                            (bit && (len == 0u || off == 0u || off > pos || pos + len > L));
             bad |= reached && b;
@@ -572,17 +615,12 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
         const uint32_t end = __shfl_sync(FULL, pos, 31);
         if (end >= L) {  // the walk ends in this step: tokens read, payload consumed
             T = tbase + __reduce_add_sync(FULL, nreach);
-            if constexpr (S == 2) {
-                if (__reduce_max_sync(FULL, lend) != L) return false;  // overrun
-                in_end = 2u * T;
-            } else {
-                const uint32_t m = __ballot_sync(FULL, nreach != 0u);
-                in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
-            }
+            const uint32_t m = __ballot_sync(FULL, nreach != 0u);
+            in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
             break;
         }
         written = end;
-        in = S == 2 ? in + 512u : __shfl_sync(FULL, pin + o, 31);  // S = 2: 256 two-byte tokens
+        in = __shfl_sync(FULL, pin + o, 31);
         tbase += 256u;
     }
     // the walk's end checks (decoder.cpp:58-65)
