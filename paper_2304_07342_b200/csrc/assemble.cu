@@ -403,15 +403,18 @@ __global__ void __launch_bounds__(kAsmWarps * 32) plz_assemble_tma_kernel(Assemb
 // warp scan of the staged sizes cuts the run into batches (chunk c joins
 // batch floor(excl_c / kAbSplit), so a batch spans at most kAbSplit plus one
 // chunk's slices) and each batch is staged by one TMA bulk copy per slice,
-// issued by the chunk's own lane on the buffer's mbarrier.  Two buffers per
-// warp: batch b + 1 is in flight while batch b is written out chunk by chunk
-// (byte head + tail in one predicated pass, realigned 128-bit body stores).
-// The next run's metadata is loaded while this run is written.
+// issued by the chunk's own lane on the buffer's mbarrier, then written out
+// chunk by chunk (byte head + tail in one predicated pass, 128-bit body
+// stores realigned from two aligned 16-byte shared loads).  One buffer per
+// warp: the other warps of the SM cover a batch's TMA latency (two buffers,
+// batch b + 1 in flight while b is written, fitted fewer warps and measured
+// 6 % slower).  The next run's metadata is loaded while this run is written.
 constexpr int kAbWarps = 4;
-constexpr uint32_t kAbSplit = 2048;
+constexpr uint32_t kAbSplit = 4096;  // c5: 2048 / 4096 / 6144 / 8192 -> 0.70 / 0.685 / 0.685 / 0.74 ms
 constexpr uint32_t kAbMaxSlices = 4608;  // C*S <= 4 KiB: + C/8 <= 512 B
 // a buffer holds kAbSplit + one chunk's largest slices (sized per launch)
-__host__ __device__ __forceinline__ uint32_t ab_warp_smem(uint32_t buf) { return 2 * buf + 16; }
+constexpr uint32_t kAbBufs = 1;  // staging buffers per warp (2: the next batch in flight)
+__host__ __device__ __forceinline__ uint32_t ab_warp_smem(uint32_t buf) { return kAbBufs * buf + 16; }
 constexpr uint64_t kAbMinChunks = 1ull << 17;  // below: the TMA ring kernel
 
 struct AbChunk {  // one chunk per lane
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
     const uint32_t lane = lane_id();
     const uint32_t warp = threadIdx.x >> 5;
     uint8_t* wbase = smem + size_t(warp) * ab_warp_smem(buf_bytes);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + 2 * buf_bytes);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(wbase + kAbBufs * buf_bytes);
     const uint32_t s_buf = static_cast<uint32_t>(__cvta_generic_to_shared(wbase));
     const uint64_t j_hi = a.j_hi ? a.j_hi : a.n_blocks;
     const uint64_t C = uint64_t(a.C), S = uint64_t(a.S);
@@ -518,7 +521,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
             const uint32_t c0 = __ffs(m) - 1, c1 = 31 - __clz(m);
             const uint32_t base = __shfl_sync(0xffffffffu, excl, c0);
             const uint32_t total = __shfl_sync(0xffffffffu, incl, c1) - base;
-            const uint32_t buf = issued & 1u;
+            const uint32_t buf = kAbBufs == 2 ? issued & 1u : 0u;
             const uint32_t s_mb = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar[buf]));
             fence_proxy_async_smem();  // earlier reads of this buffer before the TMA writes
             __syncwarp();
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
         uint32_t buf = issue(bv);
         for (;;) {
             const uint32_t bn = __reduce_min_sync(0xffffffffu, bat > bv ? bat : 0xffffffffu);
-            const uint32_t buf_n = bn != 0xffffffffu ? issue(bn) : 0u;
+            const uint32_t buf_n = kAbBufs == 2 && bn != 0xffffffffu ? issue(bn) : 0u;
             mbar_wait(&mbar[buf], (phase >> buf) & 1u);
             phase ^= 1u << buf;
             uint32_t m = __ballot_sync(0xffffffffu, bat == bv);
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(kAbWarps * 32) plz_assemble_batch_kernel(Assem
             __syncwarp();
             if (bn == 0xffffffffu) break;
             bv = bn;
-            buf = buf_n;
+            buf = kAbBufs == 2 ? buf_n : issue(bn);
         }
         cur = nxt;
     }
