@@ -415,7 +415,8 @@ constexpr uint32_t kAbMaxSlices = 4608;  // C*S <= 4 KiB: + C/8 <= 512 B
 // a buffer holds kAbSplit + one chunk's largest slices (sized per launch)
 constexpr uint32_t kAbBufs = 1;  // staging buffers per warp (2: the next batch in flight)
 __host__ __device__ __forceinline__ uint32_t ab_warp_smem(uint32_t buf) { return kAbBufs * buf + 16; }
-constexpr uint64_t kAbMinChunks = 1ull << 17;  // below: the TMA ring kernel
+constexpr uint64_t kAbMinChunks = 1ull << 14;  // below: the TMA ring kernel (c1's 4 Ki chunks: 30 vs 7.5 us;
+                                               // c2 / c3 (82 Ki / 64 Ki): 36 / 30 vs 47 / 36 us)
 
 struct AbChunk {  // one chunk per lane
     uint64_t P, F;
@@ -719,7 +720,7 @@ void launch_assemble(const AssembleArgs& a, cudaStream_t st) {
     const uint64_t slices = uint64_t(a.C) * a.S + a.C / 8 + 32;
     const int mode = assemble_mode();
     // batched runs need enough of them to fill the GPU (c5: 65k runs; c1's
-    // 128 runs took 23 us against the ring's 8 us)
+    // 128 runs took 30 us against the ring's 7.5 us)
     const uint32_t ab_slices = r16(uint32_t(a.C) * a.S) + r16(uint32_t(a.C) / 8);
     if (mode >= 2 && warps_needed >= kAbMinChunks && ab_slices <= kAbMaxSlices) {
         const uint32_t buf = kAbSplit + ab_slices;
