@@ -90,7 +90,7 @@ def test_c5_fields_sharded_equal_single_gpu():
 @pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
 @pytest.mark.parametrize("S,kind", [(1, "quant"), (2, "quant")])
 def test_batched_assembly_across_odd_containers(S, kind):
-    # Kernel III's batched runs (inputs of >= 128 Ki chunks) over containers
+    # Kernel III's batched runs (inputs of >= 16 Ki chunks) over containers
     # of 1021 chunks — runs of 32 straddle container boundaries — and a
     # partial last chunk plus (S = 2) a tail byte, against the reference image
     import inputs
