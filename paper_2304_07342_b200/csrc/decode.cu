@@ -430,25 +430,19 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
 //     into its wave's start bitmap.  Steps before the last need no
 //     reached-token bookkeeping (zero pointer fields by a zero-byte test of
 //     the packed words).
-//  B. waves of 32 output positions in order: one shared load of the wave's
-//     bitmap + token base, a popcount gives each lane its covering token, one
-//     byte load its offset, and the lane copies out[q - off] (a literal
-//     position copies onto itself).  A lane whose source is an in-wave
-//     pointer position (not final yet) follows the chain of sources through
-//     the wave's source array in shared memory — no shuffles or votes.
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
+//  B. waves of 32 output positions in order, two per step: one 16-byte
+//     shared load of both waves' bitmap + token base, a popcount gives each
+//     lane its covering token, one byte load its offset, and the lane copies
+//     out[q - off] (a literal position copies onto itself).  A lane whose
+//     source is an in-wave pointer position (not final yet) follows the
+//     chain itself through the same lookups — no shuffles or votes — and the
+//     next pair's sources are resolved before this pair's copies.
+//
+// The chunk leaves the stage as one TMA bulk store (decode_one_chunk).
 
 // Predicated shared-memory stores (no branch around them).
 __device__ __forceinline__ void st_u16_if(bool p, uint32_t a, uint32_t v) {
     asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u16 [%0], %1;\n\t}"
-                 ::"r"(a), "r"(v), "r"(uint32_t(p)) : "memory");
-}
-__device__ __forceinline__ void st_u8_if(bool p, uint32_t a, uint32_t v) {
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u8 [%0], %1;\n\t}"
                  ::"r"(a), "r"(v), "r"(uint32_t(p)) : "memory");
 }
 
