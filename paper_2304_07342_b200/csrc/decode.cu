@@ -914,6 +914,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
         }
         __syncthreads();
         if (s_stop) break;
+        __syncthreads();  // every thread has read s_stop before thread 0 rewrites it
     }
     if (tid == 0) {
         res->n_containers = s_j;
