@@ -740,7 +740,7 @@ __device__ __forceinline__ bool header_params_ok(uint32_t S, uint32_t W, uint32_
 __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
     __shared__ uint64_t s_at, s_out, s_chunks, s_j, s_n, s_maxcb;
     __shared__ unsigned long long s_bad;
-    __shared__ uint32_t s_stop, s_err;
+    __shared__ uint32_t s_stop, s_err, s_kinds;
     __shared__ uint64_t s_eoff;
     const uint32_t tid = threadIdx.x;
     ParseResult* res = a.result;
@@ -751,6 +751,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
         s_j = 0;
         s_stop = 0;
         s_maxcb = 0;
+        s_kinds = 0;
         res->err_kind = PE_OK;
     }
     __syncthreads();
@@ -906,6 +907,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
                 if (a.out)
                     for (uint64_t i = 0; i < tail; ++i) a.out[s_out + orig - tail + i] = ts[i];
                 if (C * S > s_maxcb) s_maxcb = C * S;
+                if (n) s_kinds |= S == 2 ? 2u : 1u;
                 s_at = at + need;
                 s_out += orig;
                 s_chunks += n;
@@ -921,6 +923,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
         res->total_chunks = s_chunks;
         res->total_out = s_out;
         res->max_chunk_bytes = s_maxcb;
+        res->absent_kinds = ~s_kinds & 3u;
         if (a.out_len) *a.out_len = s_out;
     }
 }
@@ -1094,6 +1097,10 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 9 : 1) p
     const uint32_t lane = lane_id();
     uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kWarpSmem;
     uint32_t* work = a.work + kKind;
+    // no container of this kernel's kind (the parse found none): nothing to
+    // draw — without this the idle instance's warps contend on its counter
+    // for ~0.12 ms at c5
+    if ((a.result->absent_kinds >> kKind) & 1u) return;
     const uint64_t total = a.result->total_chunks;
     // the container of the warp's last chunk: consecutive draws almost always
     // fall into it, so the binary search over the descriptors (a chain of

@@ -272,6 +272,10 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     pr.n_containers = descs.size();
     pr.total_chunks = total_chunks;
     pr.total_out = total_out;
+    uint32_t kinds = 0;
+    for (const ContainerDesc& d : descs)
+        if (d.num_chunks) kinds |= d.S == 2 ? 2u : 1u;
+    pr.absent_kinds = ~kinds & 3u;
     CK(cudaMemcpyAsync(c->desc.p, descs.data(), descs.size() * sizeof(ContainerDesc),
                        cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(&m->parse, &pr, sizeof pr, cudaMemcpyHostToDevice, st));
