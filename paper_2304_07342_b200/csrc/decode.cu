@@ -745,14 +745,68 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
     const uint32_t tid = threadIdx.x;
     ParseResult* res = a.result;
     if (tid == 0) {
-        s_at = 0;
-        s_out = 0;
-        s_chunks = 0;
-        s_j = 0;
         s_stop = 0;
-        s_maxcb = 0;
-        s_kinds = 0;
         res->err_kind = PE_OK;
+        // Fast chain (thread 0, no barriers): every container that passes all
+        // of read_container's checks gets its descriptor here with one round
+        // of loads — the header and, at the chunk count predicted from the
+        // previous container (every container but the last has the same),
+        // the four table words the checks and the next container's offset
+        // need.  At the first container with anything unusual (a failed
+        // check, a mispredicted count, the descriptor table full) it stops,
+        // and the exact loop below takes over from that container.
+        uint64_t at = 0, out = 0, chunks = 0, j = 0, maxcb = 0, n_pred = 0;
+        uint32_t kinds = 0;
+        while (at < a.img_len && j < a.desc_cap) {
+            const uint8_t* b = a.img + at;
+            const uint64_t size = a.img_len - at;
+            if (j == 0) n_pred = size >= 26 ? ld_le32(b + 21) : 0u;  // the first: read first
+            if (size < 26 + 8 * (n_pred + 1)) break;
+            const uint8_t* pt = b + 26;
+            const uint8_t* ftp = pt + 4 * (n_pred + 1);
+            const uint32_t p0 = ld_le32(pt), f0 = ld_le32(ftp);
+            const uint64_t ptot = ld_le32(pt + 4 * n_pred), ftot = ld_le32(ftp + 4 * n_pred);
+            const uint32_t S = b[5], W = b[6], I = b[7], C = ld_le32(b + 9), tail = b[25];
+            const uint64_t orig = ld_le64(b + 13), n = ld_le32(b + 21);
+            if (b[0] != 'P' || b[1] != 'L' || b[2] != 'Z' || b[3] != '1' || b[4] != 1 || b[8] != 0 ||
+                !header_params_ok(S, W, I, C) || tail >= S || n != n_pred || p0 != 0 || f0 != 0)
+                break;
+            const uint64_t need = 26 + 8 * (n + 1) + ftot + ptot + tail;
+            if (size < need || orig < tail || (orig - tail) % S != 0 ||
+                ((orig - tail) / S + C - 1) / C != n || out + orig > a.out_cap)
+                break;
+            ContainerDesc d;
+            d.img_off = at;
+            d.out_off = out;
+            d.chunk_base = chunks;
+            d.flags_off = at + 26 + 8 * (n + 1);
+            d.payload_off = d.flags_off + ftot;
+            d.payload_len = ptot;
+            d.original_len = orig;
+            d.num_chunks = uint32_t(n);
+            d.chunk_size = C;
+            d.last_len = n ? uint32_t((orig - tail) / S - (n - 1) * C) : 0u;
+            d.S = uint8_t(S);
+            d.W = uint8_t(W);
+            d.I = uint8_t(I);
+            d.tail_len = uint8_t(tail);
+            a.desc[j] = d;
+            if (a.out)
+                for (uint64_t i = 0; i < tail; ++i) a.out[out + orig - tail + i] = b[need - tail + i];
+            if (uint64_t(C) * S > maxcb) maxcb = uint64_t(C) * S;
+            if (n) kinds |= S == 2 ? 2u : 1u;
+            at += need;
+            out += orig;
+            chunks += n;
+            ++j;
+            n_pred = n;  // the next container's chunk count (a mispredict ends the chain)
+        }
+        s_at = at;
+        s_out = out;
+        s_chunks = chunks;
+        s_j = j;
+        s_maxcb = maxcb;
+        s_kinds = kinds;
     }
     __syncthreads();
     for (;;) {
