@@ -436,8 +436,7 @@ __device__ __forceinline__ AbChunk ab_load(const AssembleArgs& a, uint64_t g, ui
 
 // Warp copy of one staged slice: byte head to dst's 16-byte alignment and
 // byte tail in one predicated pass (lanes 0-15 head, 16-31 tail), then the
-// body as realigned 128-bit stores (five aligned shared loads, four funnel
-// shifts per word).
+// body as realigned 128-bit stores.
 __device__ __forceinline__ void ab_copy(uint8_t* dst, uint32_t src, uint32_t len, uint32_t lane) {
     const uint32_t head = min((16u - uint32_t(reinterpret_cast<uintptr_t>(dst) & 15u)) & 15u, len);
     const uint32_t body = (len - head) >> 4;
