@@ -356,32 +356,27 @@ __device__ uint32_t decode_chunk_smem(const uint8_t* __restrict__ flags, uint32_
             uint32_t before = 0;  // batch tokens starting before the wave
             uint32_t a_bm = s_bm;                       // start-bitmap word of the wave
             uint32_t a_q = s_w + lane * uint32_t(S);    // this lane's output slot
-            int wb = 0;                                 // the wave's first position
 #pragma unroll 1
             for (uint32_t w = 0; w < nw; ++w) {
                 const uint32_t starts = lds32(a_bm);
                 const int tv = int(lds32(s_tb + 4u * (before + __popc(starts & upto))));
-                // batch-relative source; negative = an earlier batch (final)
-                int src = wb + int(lane) + tv;
-                // a source inside the wave: 0 < off <= lane
-                if (__any_sync(0xffffffffu, uint32_t(-tv - 1) < lane)) {
-                    // sources inside the wave: pointer jumping over the lanes —
-                    // a lane whose source is lane r's position takes lane r's
-                    // source (a literal lane's source is itself), until every
-                    // source is final (a literal or an earlier wave)
-                    bool more;
-                    do {
-                        const bool in = src >= wb;
-                        const int s2 = __shfl_sync(0xffffffffu, src, uint32_t(src) & 31u);
-                        more = in && s2 != src;
-                        src = in ? s2 : src;
-                    } while (__any_sync(0xffffffffu, more));
+                // in-wave index of the source (< 0: an earlier wave, final).  A
+                // source inside the wave (0 < off <= lane) on a pointer position
+                // is not final yet: the lane follows the chain itself through
+                // the same lookups until a literal or an earlier wave
+                int src = int(lane) + tv;
+                if (tv != 0 && src >= 0) {
+                    for (;;) {
+                        const int t2 = int(lds32(s_tb + 4u * (before + __popc(starts & ((2u << src) - 1u)))));
+                        if (t2 == 0) break;  // a literal: written above
+                        src += t2;
+                        if (src < 0) break;
+                    }
                 }
-                sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (src - wb - int(lane)) * S)));
+                sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (src - int(lane)) * S)));
                 before += __popc(starts);
                 a_bm += 4u;
                 a_q += 32u * S;
-                wb += 32;
                 __syncwarp();
             }
         }
