@@ -546,6 +546,70 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
             in_end = 2u * T;
             break;
         }
+        if constexpr (S == 4) {
+            // A pointer is 2 payload bytes, a literal 4: the lane's 8 tokens
+            // take 32 - 2p bytes (p pointers), placed by a warp scan; token
+            // i starts 4i - 2 * (pointers before it) bytes into them.  Each
+            // field is read as two aligned words (only words that hold a
+            // stream byte) and funnel-shifted.
+            const uint32_t p = __popc(fb);
+            const uint32_t pin = in + warp_excl_scan_u32(32u - 2u * p, lane);
+            const uintptr_t pay0 = reinterpret_cast<uintptr_t>(pay);
+            const uintptr_t lim = pay0 + np;
+            uint32_t f[8];
+            uint32_t adv = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t o = pin + 4u * uint32_t(i) - 2u * uint32_t(__popc(i ? fb >> (8 - i) : 0u));
+                const uintptr_t a = pay0 + o;
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+                const uint32_t w0 = reinterpret_cast<uintptr_t>(w) < lim ? w[0] : 0u;
+                const uint32_t w1 = reinterpret_cast<uintptr_t>(w + 1) < lim ? w[1] : 0u;
+                f[i] = __funnelshift_r(w0, w1, 8u * uint32_t(a & 3u));
+                adv += ((fb >> (7 - i)) & 1u) ? (f[i] & 0xffu) : 1u;
+            }
+            uint32_t pos = written + warp_excl_scan_u32(adv, lane);
+            const uint32_t end = __shfl_sync(FULL, pos + adv, 31);
+            // tokens from position L on are not read: per token the payload
+            // bytes and the pointer fields are checked, overrun (the last
+            // reached token must end at L) and missing flag bits once
+            bool bad = false;
+            uint32_t nreach = 0, lend = 0, o_reach = 0, om0 = 0, om1 = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t bit = (fb >> (7 - i)) & 1u;
+                const uint32_t o = 4u * uint32_t(i) - 2u * uint32_t(__popc(i ? fb >> (8 - i) : 0u));
+                const uint32_t sz = bit ? 2u : 4u;
+                const uint32_t len = bit ? (f[i] & 0xffu) : 1u;
+                const uint32_t off = bit ? ((f[i] >> 8) & 0xffu) : 0u;
+                const bool reached = pos < L;
+                const bool has = pin + o + sz <= np;
+                bad |= reached & (!has | ((bit != 0u) & ((len == 0u) | (off == 0u) | (off > pos))));
+                const bool ok = reached & hf;
+                if (ok & !bit) sts_sym<4>(s_stage + 4u * pos, f[i]);
+                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
+                (i < 4 ? om0 : om1) |= off << (8 * (i & 3));
+                nreach += reached ? 1u : 0u;
+                o_reach = reached ? o + sz : o_reach;
+                pos += len;
+                lend = reached ? pos : lend;
+            }
+            if (hf)
+                asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(s_ptab + tbase + 8u * lane),
+                             "r"(om0), "r"(om1) : "memory");
+            if (__any_sync(FULL, bad)) return false;
+            if (end >= L) {  // the walk ends in this step
+                T = tbase + __reduce_add_sync(FULL, nreach);
+                if (__reduce_max_sync(FULL, lend) != L) return false;  // overrun
+                const uint32_t m = __ballot_sync(FULL, nreach != 0u);
+                in_end = __shfl_sync(FULL, pin + o_reach, 31 - __clz(m));
+                break;
+            }
+            written = end;
+            in = __shfl_sync(FULL, pin + 32u - 2u * p, 31);
+            tbase += 256u;
+            continue;
+        }
         // other widths (not dispatched here; kept generic): payload offsets
         // by a warp scan, fields byte by byte
         const uint32_t pin = in + warp_excl_scan_u32(2u * __popc(fb) + uint32_t(S) * (8u - __popc(fb)), lane);
@@ -1049,7 +1113,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
     bulk_store_drain(lane);  // the previous chunk's stage has left
-    if (kUseFast && !kExact && S == 2 && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
+    if (kUseFast && !kExact && (S == 2 || S == 4) && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
     else if (in_smem)
@@ -1120,7 +1184,7 @@ __device__ __forceinline__ uint32_t decode_desc_chunk(const DecodeArgs& a, const
                     return decode_one_chunk<2, kPipe, true>(a, d, k, stage, lane, tok, pp);
                 else
                     return TE_OK;  // not this kernel's container
-            default: return decode_one_chunk<4, kPipe, true>(a, d, k, stage, lane, tok, pp);
+            default: return decode_one_chunk<4, kPipe, kExact || kKind == kKindAll>(a, d, k, stage, lane, tok, pp);
         }
     }
 }
@@ -1140,9 +1204,9 @@ __device__ __forceinline__ uint32_t decode_global_chunk(const DecodeArgs& a, uin
 // chunk of a container the kernel does not take moves the counter past that
 // container, so the other kernel's containers cost one draw each.
 template <bool kPipe, int kKind>
-__global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 9 : 1) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
+__global__ void __launch_bounds__(kDecodeWarps * 32, 9) plz_decode_kernel(DecodeArgs a, DecodePipe pp) {
     extern __shared__ __align__(16) uint8_t smem[];
-    constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
+    constexpr uint32_t kWarpSmem = kMainWarpSmem;
     const uint32_t lane = lane_id();
     uint8_t* stage = smem + size_t(threadIdx.x >> 5) * kWarpSmem;
     uint32_t* work = a.work + kKind;
@@ -1167,7 +1231,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kKind == kKindS2 ? 9 : 1) p
             c_hi = c_lo + a.desc[cj].num_chunks;
         }
         const ContainerDesc d = a.desc[cj];
-        if ((d.S == 2) != (kKind == kKindS2)) {
+        if ((d.S == 2 ? kKindS2 : kKindOther) != kKind) {
             if (lane == 0) atomicMax(work, uint32_t(min(total, d.chunk_base + d.num_chunks)));
             continue;
         }
@@ -1287,7 +1351,7 @@ __global__ void plz_decode_one_kernel(DecodeOneArgs a) {
 namespace {
 template <bool kPipe, int kKind>
 void launch_kind(const DecodeArgs& a, const DecodePipe& pp, int sms, cudaStream_t st) {
-    constexpr uint32_t kWarpSmem = kKind == kKindS2 ? kMainWarpSmem : kDecodeWarpSmem;
+    constexpr uint32_t kWarpSmem = kMainWarpSmem;
     const size_t smem = size_t(kDecodeWarps) * kWarpSmem;
     static int per_sm = -1;  // same answer on every B200; computed once
     if (per_sm < 0) {
@@ -1339,6 +1403,7 @@ void preload_decode_kernels() {
     for (const void* f : {reinterpret_cast<const void*>(plz_parse_kernel),
                           reinterpret_cast<const void*>(plz_decode_kernel<false, kKindOther>),
                           reinterpret_cast<const void*>(plz_decode_kernel<false, kKindS2>),
+
                           reinterpret_cast<const void*>(plz_decode_kernel<true, kKindOther>),
                           reinterpret_cast<const void*>(plz_decode_kernel<true, kKindS2>),
                           reinterpret_cast<const void*>(plz_chunk_detail_kernel),

@@ -252,7 +252,7 @@ int plzgpu_decompress_range(plzgpu_ctx* c, const void* img, uint64_t len, uint64
         // the decode kernel over [cb, ce): work counter from cb, bound ce,
         // output addressed relative to the range's first byte
         const uint32_t w0[2] = {uint32_t(cb), uint32_t(cb)};  // both decode kernels' counters
-        CK(cudaMemcpyAsync(&m->work[2], w0, 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(&m->work[2], w0, sizeof w0, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(&m->parse.total_chunks, &ce, 8, cudaMemcpyHostToDevice, st));
         a.out = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(d_out) - lo);
         a.out_cap = hi;
