@@ -45,9 +45,9 @@ constexpr uint32_t kFastTokens = 1024;  // c5 chunks carry at most ~600 tokens; 
                                         // 9 CTAs/SM measured +2.9 % on c5 against 2048 and 8
 constexpr uint32_t kFastPtab = kDecodeSmem;
 constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
-// the fast path serves S = 2 chunks of at most kDecodeSmem bytes: C <= 2048
-// output positions, 64 waves
-constexpr uint32_t kFastWaves = kDecodeSmem / 2 / 32;
+// the fast path serves chunks of at most kDecodeSmem bytes: up to 4096 output
+// positions (S = 1), 128 waves
+constexpr uint32_t kFastWaves = kDecodeSmem / 32;  // S = 1: 4096 positions
 constexpr uint32_t kFastWarpSmem = kFastMeta + 8 * kFastWaves + 16;  // + the spare table pair
 static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
 constexpr bool kUseFast = true;
@@ -546,21 +546,21 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
             in_end = 2u * T;
             break;
         }
-        if constexpr (S == 4) {
-            // A pointer is 2 payload bytes, a literal 4: the lane's 8 tokens
-            // take 32 - 2p bytes (p pointers), placed by a warp scan; token
-            // i starts 4i - 2 * (pointers before it) bytes into them.  Each
+        if constexpr (S == 4 || S == 1) {
+            // A pointer is 2 payload bytes, a literal S: the lane's 8 tokens
+            // take 8S + (2 - S)p bytes (p pointers), placed by a warp scan;
+            // token i starts Si + (2 - S) * (pointers before it) bytes in.  Each
             // field is read as two aligned words (only words that hold a
             // stream byte) and funnel-shifted.
             const uint32_t p = __popc(fb);
-            const uint32_t pin = in + warp_excl_scan_u32(32u - 2u * p, lane);
+            const uint32_t pin = in + warp_excl_scan_u32(uint32_t(8 * S + (2 - S) * int(p)), lane);
             const uintptr_t pay0 = reinterpret_cast<uintptr_t>(pay);
             const uintptr_t lim = pay0 + np;
             uint32_t f[8];
             uint32_t adv = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const uint32_t o = pin + 4u * uint32_t(i) - 2u * uint32_t(__popc(i ? fb >> (8 - i) : 0u));
+                const uint32_t o = pin + uint32_t(S * i + (2 - S) * __popc(i ? fb >> (8 - i) : 0u));
                 const uintptr_t a = pay0 + o;
                 const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
                 const uint32_t w0 = reinterpret_cast<uintptr_t>(w) < lim ? w[0] : 0u;
@@ -578,15 +578,15 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const uint32_t bit = (fb >> (7 - i)) & 1u;
-                const uint32_t o = 4u * uint32_t(i) - 2u * uint32_t(__popc(i ? fb >> (8 - i) : 0u));
-                const uint32_t sz = bit ? 2u : 4u;
+                const uint32_t o = uint32_t(S * i + (2 - S) * __popc(i ? fb >> (8 - i) : 0u));
+                const uint32_t sz = bit ? 2u : uint32_t(S);
                 const uint32_t len = bit ? (f[i] & 0xffu) : 1u;
                 const uint32_t off = bit ? ((f[i] >> 8) & 0xffu) : 0u;
                 const bool reached = pos < L;
                 const bool has = pin + o + sz <= np;
                 bad |= reached & (!has | ((bit != 0u) & ((len == 0u) | (off == 0u) | (off > pos))));
                 const bool ok = reached & hf;
-                if (ok & !bit) sts_sym<4>(s_stage + 4u * pos, f[i]);
+                if (ok & !bit) sts_sym<S>(s_stage + uint32_t(S) * pos, S == 4 ? f[i] : f[i] & 0xffu);
                 atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
                 (i < 4 ? om0 : om1) |= off << (8 * (i & 3));
                 nreach += reached ? 1u : 0u;
@@ -606,7 +606,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                 break;
             }
             written = end;
-            in = __shfl_sync(FULL, pin + 32u - 2u * p, 31);
+            in = __shfl_sync(FULL, pin + uint32_t(8 * S + (2 - S) * __popc(fb)), 31);
             tbase += 256u;
             continue;
         }
@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
             if (a.out)
                 for (uint64_t i = 0; i < tail; ++i) a.out[out + orig - tail + i] = b[need - tail + i];
             if (uint64_t(C) * S > maxcb) maxcb = uint64_t(C) * S;
-            if (n) kinds |= S == 2 ? 2u : 1u;
+            if (n) kinds |= S == 2 ? 2u : S == 4 ? 4u : 1u;
             at += need;
             out += orig;
             chunks += n;
@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
                 if (a.out)
                     for (uint64_t i = 0; i < tail; ++i) a.out[s_out + orig - tail + i] = ts[i];
                 if (C * S > s_maxcb) s_maxcb = C * S;
-                if (n) s_kinds |= S == 2 ? 2u : 1u;
+                if (n) s_kinds |= S == 2 ? 2u : S == 4 ? 4u : 1u;
                 s_at = at + need;
                 s_out += orig;
                 s_chunks += n;
@@ -1036,7 +1036,7 @@ __global__ void __launch_bounds__(256) plz_parse_kernel(DecodeArgs a) {
         res->total_chunks = s_chunks;
         res->total_out = s_out;
         res->max_chunk_bytes = s_maxcb;
-        res->absent_kinds = ~s_kinds & 3u;
+        res->absent_kinds = ~s_kinds & 7u;
         if (a.out_len) *a.out_len = s_out;
     }
 }
@@ -1113,7 +1113,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
     bulk_store_drain(lane);  // the previous chunk's stage has left
-    if (kUseFast && !kExact && (S == 2 || S == 4) && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
+    if (kUseFast && !kExact && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
     else if (in_smem)
@@ -1168,7 +1168,7 @@ __device__ __forceinline__ uint64_t find_container(const ContainerDesc* desc, ui
 // every one (the exact detail path).  Two specialised kernels keep the hot
 // S = 2 instance's registers at 56 instead of the 80 the union of all widths
 // needs (which would cost a fifth of the resident warps).
-constexpr int kKindOther = 0, kKindS2 = 1, kKindAll = 2;
+constexpr int kKindOther = 0, kKindS2 = 1, kKindS4 = 2, kKindAll = 3;
 
 template <bool kPipe, bool kExact, int kKind>
 __device__ __forceinline__ uint32_t decode_desc_chunk(const DecodeArgs& a, const ContainerDesc& d,
@@ -1176,15 +1176,21 @@ __device__ __forceinline__ uint32_t decode_desc_chunk(const DecodeArgs& a, const
                                                       uint64_t* tok, const DecodePipe& pp) {
     if constexpr (kKind == kKindS2) {
         return decode_one_chunk<2, kPipe, kExact>(a, d, k, stage, lane, tok, pp);
+    } else if constexpr (kKind == kKindS4) {
+        return decode_one_chunk<4, kPipe, kExact>(a, d, k, stage, lane, tok, pp);
     } else {
         switch (d.S) {
-            case 1: return decode_one_chunk<1, kPipe, true>(a, d, k, stage, lane, tok, pp);
+            case 1: return decode_one_chunk<1, kPipe, kExact || kKind == kKindAll>(a, d, k, stage, lane, tok, pp);
             case 2:
                 if constexpr (kKind == kKindAll)
                     return decode_one_chunk<2, kPipe, true>(a, d, k, stage, lane, tok, pp);
                 else
                     return TE_OK;  // not this kernel's container
-            default: return decode_one_chunk<4, kPipe, kExact || kKind == kKindAll>(a, d, k, stage, lane, tok, pp);
+            default:
+                if constexpr (kKind == kKindAll)
+                    return decode_one_chunk<4, kPipe, true>(a, d, k, stage, lane, tok, pp);
+                else
+                    return TE_OK;  // not this kernel's container
         }
     }
 }
@@ -1231,7 +1237,7 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, 9) plz_decode_kernel(Decode
             c_hi = c_lo + a.desc[cj].num_chunks;
         }
         const ContainerDesc d = a.desc[cj];
-        if ((d.S == 2 ? kKindS2 : kKindOther) != kKind) {
+        if ((d.S == 2 ? kKindS2 : d.S == 4 ? kKindS4 : kKindOther) != kKind) {
             if (lane == 0) atomicMax(work, uint32_t(min(total, d.chunk_base + d.num_chunks)));
             continue;
         }
@@ -1372,6 +1378,7 @@ void launch_parse(const DecodeArgs& a, cudaStream_t st) {
 // only skips containers, then the S = 2 kernel does the work
 void launch_decode(const DecodeArgs& a, int sms, cudaStream_t st) {
     launch_kind<false, kKindOther>(a, DecodePipe{}, sms, st);
+    launch_kind<false, kKindS4>(a, DecodePipe{}, sms, st);
     launch_kind<false, kKindS2>(a, DecodePipe{}, sms, st);
 }
 
@@ -1382,6 +1389,7 @@ void launch_range(const DecodeArgs& a, uint64_t cb, uint64_t ce, uint8_t* out, u
 
 void launch_decode_pipelined(const DecodeArgs& a, const DecodePipe& pp, int sms, cudaStream_t st) {
     launch_kind<true, kKindOther>(a, pp, sms, st);
+    launch_kind<true, kKindS4>(a, pp, sms, st);
     launch_kind<true, kKindS2>(a, pp, sms, st);
 }
 
@@ -1403,6 +1411,8 @@ void preload_decode_kernels() {
     for (const void* f : {reinterpret_cast<const void*>(plz_parse_kernel),
                           reinterpret_cast<const void*>(plz_decode_kernel<false, kKindOther>),
                           reinterpret_cast<const void*>(plz_decode_kernel<false, kKindS2>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<false, kKindS4>),
+                          reinterpret_cast<const void*>(plz_decode_kernel<true, kKindS4>),
 
                           reinterpret_cast<const void*>(plz_decode_kernel<true, kKindOther>),
                           reinterpret_cast<const void*>(plz_decode_kernel<true, kKindS2>),

@@ -32,7 +32,7 @@ int enqueue_decompress(plzgpu_ctx* c, const uint8_t* d_img, uint64_t len, uint8_
     launch_parse(a, st);
     launch_decode(a, c->sms, st);
     CK(cudaGetLastError());
-    c->last_launches = 3;
+    c->last_launches = 4;  // parse + the three decode kernels
     c->last_op = OP_DECOMPRESS;
     c->last_decode = a;
     return PLZGPU_OK;
@@ -251,14 +251,14 @@ int plzgpu_decompress_range(plzgpu_ctx* c, const void* img, uint64_t len, uint64
     if (ce > cb) {
         // the decode kernel over [cb, ce): work counter from cb, bound ce,
         // output addressed relative to the range's first byte
-        const uint32_t w0[2] = {uint32_t(cb), uint32_t(cb)};  // both decode kernels' counters
+        const uint32_t w0[3] = {uint32_t(cb), uint32_t(cb), uint32_t(cb)};  // the decode kernels' counters
         CK(cudaMemcpyAsync(&m->work[2], w0, sizeof w0, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(&m->parse.total_chunks, &ce, 8, cudaMemcpyHostToDevice, st));
         a.out = reinterpret_cast<uint8_t*>(reinterpret_cast<uintptr_t>(d_out) - lo);
         a.out_cap = hi;
         launch_decode(a, c->sms, st);
         CK(cudaGetLastError());
-        c->last_launches = 4;
+        c->last_launches = 5;
         c->last_op = OP_DECOMPRESS;
         c->last_decode = a;
         bool grow = false;

@@ -165,7 +165,7 @@ struct Meta {
     unsigned long long err_chunk;
     unsigned long long mono_key;  // first table-monotonicity violation, ~0 if none
     uint64_t mono_base;           // first chunk of its container
-    uint32_t work[12];  // [0] first bitmap pass, [1] scan tiles, [2]/[3] the decode kernels,
+    uint32_t work[12];  // [0] first bitmap pass, [1] scan tiles, [2]/[3]/[4] the decode kernels,
                         // [4]/[6]/[8] overflow counts of the bitmap passes, [5]/[9]
                         // second/third bitmap pass, [7] wide pass
     uint32_t stalled;  // H2D pipeline: a segment never arrived

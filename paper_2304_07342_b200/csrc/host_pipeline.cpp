@@ -274,8 +274,8 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     pr.total_out = total_out;
     uint32_t kinds = 0;
     for (const ContainerDesc& d : descs)
-        if (d.num_chunks) kinds |= d.S == 2 ? 2u : 1u;
-    pr.absent_kinds = ~kinds & 3u;
+        if (d.num_chunks) kinds |= d.S == 2 ? 2u : d.S == 4 ? 4u : 1u;
+    pr.absent_kinds = ~kinds & 7u;
     CK(cudaMemcpyAsync(c->desc.p, descs.data(), descs.size() * sizeof(ContainerDesc),
                        cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(&m->parse, &pr, sizeof pr, cudaMemcpyHostToDevice, st));
@@ -339,7 +339,7 @@ int try_decompress_pipelined(plzgpu_ctx* c, const uint8_t* img, uint64_t len, ui
     CK(cudaMemcpyAsync(h, m, sizeof(Meta), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaStreamSynchronize(c->copy_stream));
-    c->last_launches = 2;
+    c->last_launches = 3;
     c->last_op = OP_DECOMPRESS;
     c->last_decode = a;
     if (h->stalled || h->err_chunk != ~0ull || h->mono_key != ~0ull) return 0;

@@ -247,7 +247,7 @@ struct ParseResult {
     uint64_t err_offset;         // byte offset relative to that container
     uint8_t hdr_S, hdr_W, hdr_I, pad0;
     uint32_t hdr_C;              // raw header fields for the validation message
-    uint32_t absent_kinds;       // bit k: no container for decode kernel kind k (0: S = 1 / 4, 1: S = 2)
+    uint32_t absent_kinds;       // bit k: no container for decode kernel kind k (0: S = 1, 1: S = 2, 2: S = 4)
     uint32_t pad1;
     uint64_t max_chunk_bytes;
 };
