@@ -22,7 +22,7 @@ img = plz.compress(torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda(), 
 assert bytes(plz.decompress_bytes(img).cpu().numpy().tobytes()) == data
 print("sanitize case ok")
 PY
-for tool in racecheck synccheck; do
+for tool in memcheck racecheck synccheck; do
   timeout 1500 compute-sanitizer --tool $tool --num-cuda-barriers 65536 --print-limit 20 python /tmp/san_case.py > gpurun_out/san_$tool.log 2>&1
   echo "$tool rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|hazard|Invalid|sanitize case" gpurun_out/san_$tool.log | head -8
 done
