@@ -383,7 +383,8 @@ def test_corrupted_images_raise_the_reference_error():
 
 
 @pytest.mark.parametrize("S,C,kind", [(2, 2048, "quant"), (2, 1024, "runs"), (2, 2048, "alpha"),
-                                       (4, 1024, "quant")])
+                                       (4, 1024, "quant"), (4, 1024, "runs"), (1, 4096, "quant"),
+                                       (1, 2048, "alpha")])
 def test_corrupted_streams_raise_the_reference_error(S, C, kind):
     # the fast chunk decoder only accepts or rejects (rejected chunks are
     # re-walked for the exact error): corruptions of the flag / payload
