@@ -484,8 +484,10 @@ template <int S>
 __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_t* lists,
                                                            uint64_t stride, uint32_t* counts) {
     __shared__ uint32_t seen[4][8];
+    __shared__ uint32_t lane_seen[4][8 * 32];  // per lane: 256-bit presence set, word w at [w * 32 + lane]
     const uint32_t lane = lane_id();
     uint32_t* bm = seen[threadIdx.x >> 5];
+    const uint32_t s_ls = static_cast<uint32_t>(__cvta_generic_to_shared(lane_seen[threadIdx.x >> 5])) + 4u * lane;
     const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
     for (uint64_t ck = uint64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
          ck < a.n_chunks; ck += warps) {
@@ -498,7 +500,12 @@ __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_
             if (n == a.C && n <= 4096 && a.bulk_ok) {
                 // whole chunk of at most 4 KiB, 16-byte aligned: every lane's
                 // 16-byte words loaded up front (one memory round trip per
-                // chunk instead of one per 128 bytes)
+                // chunk), each lane's bytes into its own 256-bit set in shared
+                // memory (conflict-free: word w of lane l at w * 32 + l; no
+                // warp-wide match per byte), the 32 sets OR-reduced at the end
+#pragma unroll
+                for (int w = 0; w < 8; ++w)
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(s_ls + 128u * w), "r"(0u) : "memory");
                 uint4 v[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
@@ -508,31 +515,42 @@ __global__ void __launch_bounds__(128) plz_classify_kernel(EncodeArgs a, uint32_
                     if (512 * k >= n) break;
                     const uint32_t w4[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
 #pragma unroll
-                    for (int b = 0; b < 16; ++b) {  // one atomic per distinct value of the warp
+                    for (int b = 0; b < 16; ++b) {
                         const uint32_t x = (w4[b >> 2] >> (8 * (b & 3))) & 0xffu;
+                        const uint32_t ad = s_ls + 128u * (x >> 5);
+                        uint32_t m;
+                        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(ad) : "memory");
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ad), "r"(m | (1u << (x & 31u))) : "memory");
+                    }
+                }
+                uint32_t tot = 0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w) {
+                    uint32_t m;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(m) : "r"(s_ls + 128u * w) : "memory");
+                    tot += __popc(__reduce_or_sync(0xffffffffu, m));
+                }
+                D = int(tot);
+            } else {
+                for (int base = 0; base < n; base += 128) {  // uniform trip count (match_any)
+                    const int i = base + 4 * static_cast<int>(lane);
+                    uint32_t v;
+                    if (i + 4 <= n && a.bulk_ok) {  // the input base is 16-byte aligned
+                        v = *reinterpret_cast<const uint32_t*>(src + i);
+                    } else {  // past the chunk: repeat its first byte, a no-op for the set
+                        v = 0;
+                        for (int b = 0; b < 4; ++b) v |= uint32_t(i + b < n ? src[i + b] : src[0]) << (8 * b);
+                    }
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {  // one atomic per distinct value of the warp
+                        const uint32_t x = (v >> (8 * b)) & 0xffu;
                         const uint32_t same = __match_any_sync(0xffffffffu, x);
                         if (__ffs(same) - 1 == static_cast<int>(lane)) atomicOr(&bm[x >> 5], 1u << (x & 31u));
                     }
                 }
-            } else
-            for (int base = 0; base < n; base += 128) {  // uniform trip count (match_any)
-                const int i = base + 4 * static_cast<int>(lane);
-                uint32_t v;
-                if (i + 4 <= n && a.bulk_ok) {  // the input base is 16-byte aligned
-                    v = *reinterpret_cast<const uint32_t*>(src + i);
-                } else {  // past the chunk: repeat its first byte, a no-op for the set
-                    v = 0;
-                    for (int b = 0; b < 4; ++b) v |= uint32_t(i + b < n ? src[i + b] : src[0]) << (8 * b);
-                }
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {  // one atomic per distinct value of the warp
-                    const uint32_t x = (v >> (8 * b)) & 0xffu;
-                    const uint32_t same = __match_any_sync(0xffffffffu, x);
-                    if (__ffs(same) - 1 == static_cast<int>(lane)) atomicOr(&bm[x >> 5], 1u << (x & 31u));
-                }
+                __syncwarp();
+                D = int(__reduce_add_sync(0xffffffffu, lane < 8 ? __popc(bm[lane]) : 0u));
             }
-            __syncwarp();
-            D = int(__reduce_add_sync(0xffffffffu, lane < 8 ? __popc(bm[lane]) : 0u));
             __syncwarp();
         } else {
             D = count_alphabet<S>(a.in + ck * uint64_t(a.C) * S, n, lane);
