@@ -508,7 +508,7 @@ def run_b200(args):
             int_peaks[name] = v.value
     nw = [1, 2, 4, 8][(w.W > 32) + (w.W > 64) + (w.W > 128)]
     prof = ncu_profile_facts(f"plz_bitmatch_kernel<{w.S}, {nw}, 12>")
-    dprof = ncu_profile_facts("plz_decode_kernel")
+    dprof = ncu_profile_facts("plz_decode_kernel<0, 1>")  # the S = 2 instance (c5)
     pairs = match_pairs(n, w)
     pairs_s = pairs / (enc_ms * 1e-3)
     lane_peak = int_peaks.get("lop3")

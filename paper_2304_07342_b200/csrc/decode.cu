@@ -36,19 +36,32 @@ constexpr uint32_t kDecodePad = 128;
 constexpr uint32_t kDecodeWarpSmem = kDecodeSmem + kDecodePad + 144 + kDecodeSmem / 8;
 // The decode kernel's per-warp region (decode_chunk_fast): output stage
 // (kDecodeSmem bytes), token table (one byte per token: a pointer's offset,
-// 0 for a literal; kFastTokens entries — a chunk with more flag bits than
-// that takes decode_chunk_smem), wave table (per 32 output positions:
+// 0 for a literal; fast_tokens<S>() entries — a chunk with more flag bits
+// than that takes decode_chunk_smem), wave table (per 32 output positions:
 // token-start bitmap + address of the token before the wave; read two
 // entries at a time, so one spare entry).
-constexpr uint32_t kFastTokens = 1024;  // c5 chunks carry at most ~600 tokens; a chunk with more
-                                        // (over half literals) takes decode_chunk_smem.  1024 and
-                                        // 9 CTAs/SM measured +2.9 % on c5 against 2048 and 8
+constexpr uint32_t kFastTokens = 1024;  // S = 1 (c5 chunks carry at most ~600 tokens); the
+                                        // region for 1024 and 9 CTAs/SM measured +2.9 % on c5
+                                        // against 2048 and 8
 constexpr uint32_t kFastPtab = kDecodeSmem;
 constexpr uint32_t kFastMeta = kFastPtab + kFastTokens;
 // the fast path serves chunks of at most kDecodeSmem bytes: up to 4096 output
 // positions (S = 1), 128 waves
 constexpr uint32_t kFastWaves = kDecodeSmem / 32;  // S = 1: 4096 positions
 constexpr uint32_t kFastWarpSmem = kFastMeta + 8 * kFastWaves + 16;  // + the spare table pair
+// Per width, the wave table needs only kDecodeSmem / (32 S) entries; the
+// token table takes the rest of the region (S = 2: 1536 tokens, so chunks of
+// up to 75 % literals — I = 16 streams — stay on the fast path; S = 1: 1024).
+// The spare pair after a width's last wave also takes phase A's dump bits.
+template <int S>
+__host__ __device__ constexpr uint32_t fast_waves() { return kDecodeSmem / (32u * S); }
+template <int S>
+__host__ __device__ constexpr uint32_t fast_tokens() {
+    return kFastWarpSmem - 16u - 8u * fast_waves<S>() - kFastPtab;
+}
+static_assert(fast_tokens<1>() == kFastTokens && fast_tokens<2>() == 1536u, "fast layout");
+static_assert((kFastPtab + fast_tokens<2>()) % 16u == 0 && (kFastPtab + fast_tokens<4>()) % 16u == 0,
+              "wave table alignment (read as uint4 pairs)");
 static_assert(kFastWarpSmem >= kDecodeWarpSmem, "the exact path shares the warp's region");
 constexpr bool kUseFast = true;
 constexpr uint32_t kMainWarpSmem = kUseFast ? kFastWarpSmem : kDecodeWarpSmem;
@@ -450,7 +463,8 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                                   const uint8_t* __restrict__ pay, uint32_t np, uint32_t L,
                                   uint8_t* wsm, uint32_t lane) {
     constexpr uint32_t FULL = 0xffffffffu;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastMeta);  // pairs {starts, base}
+    uint32_t* meta = reinterpret_cast<uint32_t*>(wsm + kFastPtab + fast_tokens<S>());  // pairs {starts, base}
+    constexpr uint32_t kDump = 2u * fast_waves<S>();  // the spare pair: bits of unreached tokens
     const uint32_t s_stage = static_cast<uint32_t>(__cvta_generic_to_shared(wsm));
     const uint32_t s_ptab = s_stage + kFastPtab;
     const uint32_t nwv = (L + 31u) >> 5;
@@ -493,7 +507,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
             uint32_t pos = written + warp_excl_scan_u32(adv, lane);
             const uint32_t end = __shfl_sync(FULL, pos + adv, 31);
             // token table: the 8 offsets at once (tokens past the flag bytes
-            // are never stored: that bounds the table, 8 * nf <= kFastTokens)
+            // are never stored: that bounds the table, 8 * nf <= fast_tokens<S>())
             if (hf)
                 asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(s_ptab + tbase + 8u * lane),
                              "r"(om0), "r"(om1) : "memory");
@@ -535,7 +549,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                 bad |= reached & ((len == 0u) | ((bit != 0u) & (off == 0u)) | (off > pos));
                 const bool ok = reached & hf;
                 st_u16_if(ok & !bit, s_stage + 2u * pos, fld);
-                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
+                atomicOr(&meta[ok ? 2u * (pos >> 5) : kDump], 1u << (pos & 31u));
                 nreach += reached ? 1u : 0u;
                 pos += len;
                 lend = reached ? pos : lend;
@@ -587,7 +601,7 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
                 bad |= reached & (!has | ((bit != 0u) & ((len == 0u) | (off == 0u) | (off > pos))));
                 const bool ok = reached & hf;
                 if (ok & !bit) sts_sym<S>(s_stage + uint32_t(S) * pos, S == 4 ? f[i] : f[i] & 0xffu);
-                atomicOr(&meta[ok ? 2u * (pos >> 5) : 2u * kFastWaves], 1u << (pos & 31u));
+                atomicOr(&meta[ok ? 2u * (pos >> 5) : kDump], 1u << (pos & 31u));
                 (i < 4 ? om0 : om1) |= off << (8 * (i & 3));
                 nreach += reached ? 1u : 0u;
                 o_reach = reached ? o + sz : o_reach;
@@ -1113,7 +1127,7 @@ __device__ __forceinline__ uint32_t decode_one_chunk(const DecodeArgs& a, const 
     uint32_t e;
     uint32_t* tab = reinterpret_cast<uint32_t*>(stage + kDecodeSmem + kDecodePad);
     bulk_store_drain(lane);  // the previous chunk's stage has left
-    if (kUseFast && !kExact && in_smem && 8u * uint64_t(f1 - f0) <= kFastTokens)
+    if (kUseFast && !kExact && in_smem && 8u * uint64_t(f1 - f0) <= fast_tokens<S>())
         e = decode_chunk_fast<S>(fl, f1 - f0, py, p1 - p0, uint32_t(L), stage, lane)
                 ? TE_OK : TE_FLAGS_EXHAUSTED;
     else if (in_smem)

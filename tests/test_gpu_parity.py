@@ -101,6 +101,31 @@ def test_configs_bit_exact(S, W, C, I, kind):
     assert plz.decompress_bytes(got) == data
 
 
+@pytest.mark.parametrize("I", [1, 16])
+def test_decode_token_table_boundaries(I):
+    # the fast decode holds one byte per token: S = 2 chunks with up to 1536
+    # tokens decode there, more (mostly literals) through decode_chunk_smem;
+    # chunks whose literal share steps across 1024 / 1536 / 2048 tokens
+    rng = random.Random(1536 + I)
+    C, chunks = 2048, []
+    for k in range(40):
+        frac = 0.3 + 0.7 * k / 39  # share of random (literal) symbols
+        sym = []
+        while len(sym) < C:
+            if rng.random() < frac:
+                sym.append(rng.randrange(65536))
+            else:
+                sym.extend([7, 7, 9, 7, 9, 9][: rng.randrange(2, 7)])
+        chunks.append(b"".join(v.to_bytes(2, "little") for v in sym[:C]))
+    data = b"".join(chunks) + b"\x05\x06" * 333
+    p = P(2, 255, C, I)
+    want, _ = ref_compress(data, p)
+    got = plz.compress(data, p)
+    assert got == want
+    assert plz.decompress_bytes(got) == data
+    assert ref_decompress(got) == data
+
+
 @pytest.mark.parametrize("S,C", [(2, 2048), (2, 1024), (4, 1024), (4, 4096)])
 def test_alphabet_tier_boundaries(S, C):
     # Kernel I's bitmap passes keep one occurrence row per distinct symbol of

@@ -1,12 +1,12 @@
-"""Every BASELINE.json config on one B200 (bench.py's headline is c2):
+"""Every BASELINE.json config on one B200 (bench.py's headline is c5):
 
     python tools/config_sweep.py [--steps 5] [--configs c1,c2,c3,c4,c5] [--cpu]
 
 c1  u8 16 MiB, W=128, I=1           (the reference's CPU-runnable case)
-c2  u16 CESM-like, W=255, I=2       (bench.py's workload)
+c2  u16 CESM-like, W=255, I=2
 c3  u16 NYX-like 512^3, W=255, I in {1,2,4,8,16}: ratio vs throughput
 c4  u32 1 GiB, W=255, I=4           (decompression focus)
-c5  u16 8 GiB (32 NYX-like fields), W=255, I=2, one GPU
+c5  u16 8 GiB (32 NYX-like fields), W=255, I=2, one GPU (bench.py's workload)
 
 One JSON line per (config, I): compress / decompress GB/s of input bytes
 (device-resident, CUDA events, warm-up first, inputs > L2 except c1), ratio,
