@@ -22,6 +22,6 @@ done
 # the decode kernel instance that takes the S = 2 containers (<kPipe = 0, kKindS2 = 1>; the
 # other widths' instances only return), of the second decompress call
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-    -k 'regex:plz_decode_kernel<(0|false), 1>' -s 1 -c 1 \
+    -k 'regex:plz_decode_kernel<[^>]*0, [^>]*1>' -s 1 -c 1 \
     -o gpurun_out/prof_plz_decode_kernel_$R python tools/probe.py $W 1 > /dev/null 2>&1
 ls -la gpurun_out
