@@ -749,29 +749,57 @@ __device__ bool decode_chunk_fast(const uint8_t* __restrict__ flags, uint32_t nf
             s0 = source(m.x, m.y, off0);
             s1 = source(m.z, m.w, off1);
         }
-        __syncwarp();  // converged (and the previous pair's stores visible) before the copies
     };
     // A wave's copy reads what the previous wave's copy stored.  The warp is
-    // converged from the __syncwarp that ends each sources() (and before the
-    // single tail wave) through both copies of a pair — straight-line code —
-    // so the stores of one warp-wide st.shared are visible to the next
+    // converged from the __syncwarp that follows each group's sources()
+    // (where the chase may diverge) through the group's copies — straight-line
+    // code — so the stores of one warp-wide st.shared are visible to the next
     // warp-wide ld.shared without a barrier per wave; only the compiler is
-    // kept from reordering them (volatile asm + memory clobber).  The
-    // per-wave __syncwarp() (a divergence check, UMOV + BRA.DIV, per wave)
-    // cost 3.9 % of c5's decompress.
+    // kept from reordering them (volatile asm + memory clobber).  A
+    // __syncwarp() per wave (a divergence check, UMOV + BRA.DIV, each) cost
+    // 3.9 % of c5's decompress; one per pair 1.7 %, one per four waves ~1.2 %.
     auto copy = [&](int s) {
         sts_sym<S>(a_q, lds_sym<S>(uint32_t(int(a_q) + (s - int(lane)) * S)));
         a_q += 32u * S;
         asm volatile("" ::: "memory");
     };
     uint32_t w = 0;
-    if (nwv >= 2u) {
-        int s0, s1;
+    // S = 2: groups of four waves, one warp barrier per group (the S = 1 and
+    // S = 4 instances spill with four sources live and take pairs)
+    if (S == 2 && nwv >= 4u) {
+        int s0, s1, s2, s3;
         sources(meta4[0], s0, s1);
+        sources(meta4[1], s2, s3);
+        __syncwarp();
+        for (; w + 8u <= nwv; w += 4u) {
+            int n0, n1, n2, n3;
+            sources(meta4[(w >> 1) + 2u], n0, n1);
+            sources(meta4[(w >> 1) + 3u], n2, n3);
+            __syncwarp();  // converged, and the previous group's stores visible
+            copy(s0);
+            copy(s1);
+            copy(s2);
+            copy(s3);
+            s0 = n0;
+            s1 = n1;
+            s2 = n2;
+            s3 = n3;
+        }
+        copy(s0);
+        copy(s1);
+        copy(s2);
+        copy(s3);
+        w += 4u;
+    }
+    if (w + 2u <= nwv) {
+        int s0, s1;
+        sources(meta4[w >> 1], s0, s1);
+        __syncwarp();  // converged, and the previous pair's stores visible
 #pragma unroll 2
         for (; w + 4u <= nwv; w += 2u) {
             int n0, n1;
             sources(meta4[(w >> 1) + 1u], n0, n1);
+            __syncwarp();
             copy(s0);
             copy(s1);
             s0 = n0;
